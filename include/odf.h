@@ -1,0 +1,159 @@
+/*
+ * odf.h -- C ABI of the B200-native oblivious-decision-forest scorer.
+ *
+ * The method (arxiv 2205.07307, /root/reference/PAPER.md, cited P:<line>):
+ * a forest of oblivious trees; a tree of height d has d node conditions
+ * FACTOR[INDEX_l] < THRESHOLD_l, one per level, and 2^d answers.
+ * Scoring a document has two stages:
+ *   binarization  - evaluate the node conditions (binary features), §5;
+ *   tree apply    - per tree, write the level conditions as a binary number
+ *                   (true = 1; level l = bit l, least significant
+ *                   first), fetch that answer and sum over trees.
+ * The binarized form used here is the north_star's: per used feature f, the
+ * sorted unique thresholds ("borders") b_0 < ... < b_{m-1} and the uint8 bin
+ *   bin(x) = #{ j : !(x < b_j) }                        (0 <= bin <= m <= 254)
+ * for which  x < b_k  <=>  bin(x) <= k  for every border, NaN included
+ * (DESIGN.md "Readings of the paper").
+ *
+ * Conventions for every call:
+ *  - Host pointers are marked h_*, device pointers d_*; "stream" is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Calls are stream-ordered and asynchronous unless stated; none but
+ *    odf_load_model / odf_free_model / odf_score_host synchronises.
+ *  - The caller owns every d_* / h_* buffer; the library never frees them and
+ *    never allocates per call (odf_score_host uses model-owned staging that is
+ *    allocated once, see there).
+ *  - Errors: every call returns an odf_status; odf_last_error() returns a
+ *    thread-local message naming the violated bound.  No exceptions cross the
+ *    ABI.  A CUDA launch error is ODF_E_CUDA.  There is no CPU fallback.
+ *  - A model is immutable after load; concurrent calls on different streams
+ *    with different output buffers are safe.
+ */
+#ifndef ODF_H
+#define ODF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ODF_API __attribute__((visibility("default")))
+#else
+#define ODF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct odf_model odf_model; /* opaque */
+
+typedef enum {
+    ODF_OK = 0,
+    ODF_E_INVALID_ARG = 1, /* a documented bound is violated (message names it) */
+    ODF_E_UNSUPPORTED = 2, /* valid but outside this build's limits (>254 borders, smem) */
+    ODF_E_NOMEM = 3,       /* device or pinned-host allocation failed */
+    ODF_E_CUDA = 4         /* CUDA runtime / launch error (message has cudaGetErrorString) */
+} odf_status;
+
+/* Bins are stored in a blocked layout: tiles of ODF_TILE_DOCS documents; tile
+ * g holds n_used rows of ODF_TILE_DOCS bytes, row u = used feature u (ascending
+ * raw feature id), byte j = document g*ODF_TILE_DOCS + j.  Bytes of padding
+ * documents (>= n_docs) in the last tile are defined but meaningless.        */
+#define ODF_TILE_DOCS 128
+#define ODF_MAX_DEPTH 10
+#define ODF_MAX_BORDERS 254
+
+ODF_API int odf_version(void);                 /* ODF_VERSION_MAJOR*10000 + MINOR*100 + PATCH */
+ODF_API const char *odf_last_error(void);      /* thread-local; "" when the last call succeeded */
+
+/* Load (compile) a uniform-depth oblivious forest onto device `device`.
+ *   feature_index [n_trees*depth]  host, int32; entry t*depth + l is the factor
+ *                  tested at level l of tree t (l = 0 is the root level and bit 0
+ *                  of the leaf index); 0 <= value < n_features.
+ *   thresholds    [n_trees*depth]  host, fp32, finite; condition is
+ *                  factor < threshold (strict).
+ *   leaf_values   [n_trees << depth] host, fp32, finite; answer j of tree t at
+ *                  t*2^depth + j (P:305 with fp32 answers).
+ *   depth in [0, ODF_MAX_DEPTH]; n_trees >= 0; n_features >= 1.
+ * The arrays are copied; the caller may free them on return.  Errors:
+ *   ODF_E_INVALID_ARG  bad depth / counts / null pointer / feature index out of
+ *                      range / non-finite threshold or leaf;
+ *   ODF_E_UNSUPPORTED  a feature with more than ODF_MAX_BORDERS distinct
+ *                      thresholds, or a model whose per-tile state exceeds the
+ *                      227 KB shared-memory budget (message says which);
+ *   ODF_E_NOMEM / ODF_E_CUDA.  Synchronises the device.  *out = NULL on error. */
+ODF_API odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
+                          const float *leaf_values, int32_t depth, int64_t n_trees,
+                          int32_t n_features, int device, odf_model **out);
+
+ODF_API void odf_free_model(odf_model *m); /* NULL is a no-op; synchronises the device */
+
+typedef struct {
+    int32_t depth, n_features, n_used_features, n_split_features, n_columns;
+    int64_t n_trees;
+    int32_t trees_per_chunk, n_tree_chunks;
+    int64_t chunk_bytes, model_device_bytes;
+    int32_t max_borders;        /* max distinct borders of one feature */
+    int64_t total_borders;      /* sum over used features */
+    int32_t borders_in_smem;    /* 1 if the fused kernel keeps all borders in shared memory */
+    int32_t stages_fused;       /* ring stages of the fused kernel */
+    int32_t smem_fused;         /* dynamic shared memory per CTA of the fused kernel, bytes */
+    int32_t num_sms;
+} odf_model_info;
+
+ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);
+
+/* Bytes of the blocked bins buffer for n_docs documents
+ * (= ceil(n_docs/ODF_TILE_DOCS) * n_used * ODF_TILE_DOCS), the number of used
+ * features, and (optional, may be NULL) a library-owned pointer to their raw
+ * ids, ascending, valid until odf_free_model.                                */
+ODF_API odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
+                           int32_t *n_used_features, const int32_t **used_feature_ids);
+
+/* Stage 1 (§5): d_factors [n_docs x ld] fp32 row-major on the
+ * model's device (16-byte aligned, ld % 4 == 0, ld >= n_features) -> d_bins in
+ * the blocked layout above (odf_bins_layout bytes).  n_docs == 0 is a no-op.
+ * Errors: ODF_E_INVALID_ARG (null / misaligned / ld), ODF_E_CUDA.            */
+ODF_API odf_status odf_binarize(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                        uint8_t *d_bins, void *stream);
+
+/* Stage 2 (§6): d_bins (blocked layout) -> d_scores [n_docs] fp32,
+ * score(i) = sum over trees of the answer at the tree's leaf index,
+ * accumulated in fp32 in the fixed order of DESIGN.md "Summation order"
+ * (independent of n_docs and of the document's position). n_trees == 0 -> 0. */
+ODF_API odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                     float *d_scores, void *stream);
+
+/* Fused stages 1+2 (any binarization composes with any apply): same
+ * inputs as odf_binarize, same scores as odf_apply (bit-identical: same
+ * summation order); bins live only in shared memory, never in HBM.           */
+ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                     float *d_scores, void *stream);
+
+/* Test/debug (K6): leaf indices idx[d][t] (true index, level l = bit l) of
+ * documents [doc0, doc0+ndoc) and trees [tree0, tree0+ntree) from d_bins
+ * (n_docs documents, blocked layout) into d_idx [ndoc x ntree] uint16 row-major.
+ * Computed by the same device code as odf_apply.  Errors: ranges outside
+ * [0, n_docs) x [0, n_trees) -> ODF_E_INVALID_ARG.                          */
+ODF_API odf_status odf_leaf_indices(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                            int64_t doc0, int64_t ndoc, int64_t tree0, int64_t ntree,
+                            uint16_t *d_idx, void *stream);
+
+/* Test/debug (K6): per-document FNV-1a-64 over (idx[i][0..n_trees-1]) as u16
+ * little-endian, from d_bins; d_fp [n_docs] uint64.                          */
+ODF_API odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                                 uint64_t *d_fp, void *stream);
+
+/* End-to-end from HOST memory: h_factors [n_docs x ld] fp32 (pinned or not;
+ * pinned is faster) -> h_scores [n_docs].  Copies host->device, runs the fused
+ * kernel, copies back, in chunks pipelined over two model-owned device staging
+ * buffers (allocated on first use, sized for `chunk_docs` rows of ld floats,
+ * reused while ld <= the first call's ld; freed by odf_free_model).  Blocks
+ * until h_scores is written.  Same results as odf_score.                     */
+ODF_API odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,
+                          float *h_scores, int64_t chunk_docs, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODF_H */

@@ -1,0 +1,651 @@
+// odf_capi.cu -- the C ABI (include/odf.h): model compiler (K0), validation,
+// shared-memory planning, TMA descriptor encoding and kernel launches.
+//
+// Model compile (K0), from the raw arrays of the paper's problem statement
+// (P:80 node conditions, P:301-305 per-tree conditions and answers):
+//  * used factors: every f with at least one node condition, ascending id;
+//  * borders_f = sorted unique-by-== thresholds on f (-0.0 == +0.0);
+//    m_f <= 254 so bins fit in uint8 (BASELINE.json north_star);
+//  * node (t,l) -> k = position of its threshold in borders_f (exact ==);
+//    condition x < thr  <=>  bin(x) <= k  <=>  NOT(bin >= k+1);
+//  * 7-bit code columns: column A of f holds min(bin,127); factors with
+//    m_f > 127 also get column B = max(bin-127, 0); a node tests
+//    "code >= K" on column A with K = k+1 when k+1 <= 127, else on column B
+//    with K = k-126;  descriptor = {col*128, (128-K)*0x01010101};
+//  * leaf tables reversed (table[F] = leaf[2^d-1-F]) because the kernels
+//    assemble the complemented index F (flags are "condition false");
+//  * trees grouped in chunks of tc (multiple of 16) = [descriptors | tables].
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <memory>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "../../include/odf.h"
+#include "odf_internal.h"
+
+using namespace odf;
+
+namespace {
+
+thread_local std::string g_err;
+
+odf_status fail(odf_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+odf_status fail(odf_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+odf_status ok()
+{
+    g_err.clear();
+    return ODF_OK;
+}
+odf_status cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(ODF_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+uint32_t align_up(uint64_t v, uint64_t a) { return static_cast<uint32_t>((v + a - 1) / a * a); }
+
+struct Plan {
+    uint32_t off_bins = 0, off_borders = 0, off_ring = 0, off_red = 0, off_bars = 0;
+    uint32_t slot_bytes = 0;
+    int stages = 0, fsub = 1;
+    bool bsm = false;
+    size_t smem = 0;
+    int grid_per_sm = 1;
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+}  // namespace
+
+struct odf_model {
+    int device = 0, num_sms = 0, max_smem = 0;
+    int32_t depth = 0, n_features = 0;
+    int64_t n_trees = 0;
+    std::vector<int32_t> used_ids;
+    int32_t n_used = 0, n_split = 0, n_cols = 0;
+    int32_t max_borders = 0;
+    int64_t total_borders = 0;
+    int32_t n_fchunks = 0, border_floats = 0;
+    int32_t tc = 16, n_tchunks = 0;
+    uint32_t chunk_bytes = 0, desc_bytes = 0, table_stride = 0;
+    int64_t dev_bytes = 0;
+    uint4 *d_fmeta = nullptr;
+    float *d_borders = nullptr;
+    uint8_t *d_chunks = nullptr;
+    uint2 *d_splits = nullptr;
+    Plan fused, binz, apply;
+    // odf_score_host staging
+    std::mutex host_mu;
+    float *d_stage[2] = {nullptr, nullptr};
+    float *d_sstage[2] = {nullptr, nullptr};
+    int64_t stage_rows = 0, stage_ld = 0;
+    cudaStream_t hs[2] = {nullptr, nullptr};
+    cudaEvent_t ev_in = nullptr, ev_out[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// shared-memory plans
+// ----------------------------------------------------------------------------
+bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
+{
+    const uint32_t cols = (mode == MODE_BINARIZE) ? m.n_used : m.n_cols;
+    const uint32_t bins = align_up(static_cast<uint64_t>(cols) * kTile, 1024);
+    const uint32_t red = (mode == MODE_BINARIZE) ? 0 : kRedBytes;
+    const uint32_t bars = 256;
+    const uint32_t borders = align_up(static_cast<uint64_t>(m.border_floats) * 4, 128);
+    uint32_t slot;
+    int smax;
+    if (mode == MODE_BINARIZE) {
+        slot = kFSubBytes;
+        smax = 8;
+    } else if (mode == MODE_APPLY) {
+        slot = align_up(m.chunk_bytes, 1024);
+        smax = 4;
+    } else {
+        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), kFSubBytes);
+        smax = 4;
+    }
+    const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
+    const int64_t fixed = static_cast<int64_t>(bins) + red + bars;
+    const bool want_borders = (mode != MODE_APPLY) && m.border_floats > 0;
+    int s_bsm = want_borders ? static_cast<int>((avail - fixed - borders) / slot) : -1;
+    int s_glb = static_cast<int>((avail - fixed) / slot);
+    pl.bsm = want_borders && s_bsm >= 3;
+    pl.stages = std::min(smax, pl.bsm ? s_bsm : s_glb);
+    if (pl.stages < 2) {
+        char b[256];
+        snprintf(b, sizeof b,
+                 "shared memory: %u code columns x 128 B + %u B slots do not fit %d B "
+                 "(need >= 2 slots)",
+                 cols, slot, m.max_smem);
+        why = b;
+        return false;
+    }
+    pl.slot_bytes = slot;
+    pl.fsub = static_cast<int>(slot / kFSubBytes);
+    if (pl.fsub < 1) pl.fsub = 1;
+    uint32_t off = 0;
+    pl.off_ring = off;                    // ring first: TMA swizzle needs 1024 B alignment
+    off += pl.stages * slot;
+    pl.off_bins = off;
+    off += bins;
+    pl.off_borders = off;
+    if (pl.bsm) off += borders;
+    pl.off_red = off;
+    off += red;
+    pl.off_bars = off;
+    off += bars;
+    pl.smem = off + 1024;
+    return true;
+}
+
+odf_status encode_tmap(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld,
+                       CUtensorMap *tm)
+{
+    std::call_once(g_encode_once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!g_encode) return fail(ODF_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(m->n_features), static_cast<cuuint64_t>(n_docs)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kFSub), static_cast<cuuint32_t>(kTile)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(d_x), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ODF_E_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+    return ODF_OK;
+}
+
+KParams base_params(const odf_model *m, const Plan &pl)
+{
+    KParams p;
+    memset(&p, 0, sizeof p);
+    p.fmeta = m->d_fmeta;
+    p.borders = m->d_borders;
+    p.n_fchunks = m->n_used > 0 ? m->n_fchunks : 0;
+    p.border_floats = m->border_floats;
+    p.chunks = m->d_chunks;
+    p.n_tchunks = m->n_tchunks;
+    p.tc = m->tc;
+    p.n_trees = m->n_trees;
+    p.chunk_bytes = m->chunk_bytes;
+    p.desc_bytes = m->desc_bytes;
+    p.table_stride = m->table_stride;
+    p.splits = m->d_splits;
+    p.n_split = m->n_split;
+    p.n_used = m->n_used;
+    p.n_cols = m->n_cols;
+    p.off_bins = pl.off_bins;
+    p.off_borders = pl.off_borders;
+    p.off_ring = pl.off_ring;
+    p.off_red = pl.off_red;
+    p.off_bars = pl.off_bars;
+    p.slot_bytes = pl.slot_bytes;
+    p.stages = pl.stages;
+    p.fsub_per_job = pl.fsub;
+    p.borders_smem = pl.bsm ? 1 : 0;
+    return p;
+}
+
+odf_status check_factors(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld)
+{
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs >= (int64_t(1) << 31) - kTile)
+        return fail(ODF_E_INVALID_ARG, "n_docs >= 2^31 - 128 (TMA coordinate range)");
+    if (ld < m->n_features) return fail(ODF_E_INVALID_ARG, "ld (%lld) < n_features (%d)", (long long)ld, m->n_features);
+    if (ld % 4 != 0) return fail(ODF_E_INVALID_ARG, "ld %% 4 != 0 (rows must be 16-byte aligned for TMA)");
+    if (n_docs > 0 && !d_x) return fail(ODF_E_INVALID_ARG, "d_factors is NULL");
+    if (reinterpret_cast<uintptr_t>(d_x) % 16 != 0) return fail(ODF_E_INVALID_ARG, "d_factors not 16-byte aligned");
+    return ODF_OK;
+}
+
+int grid_for(const odf_model *m, const Plan &pl, int64_t n_tiles)
+{
+    const int64_t g = static_cast<int64_t>(m->num_sms) * pl.grid_per_sm;
+    return static_cast<int>(std::min<int64_t>(n_tiles, g));
+}
+
+}  // namespace
+
+// ============================================================================
+// ABI
+// ============================================================================
+extern "C" {
+
+int odf_version(void) { return 100; }
+const char *odf_last_error(void) { return g_err.c_str(); }
+
+void odf_free_model(odf_model *m)
+{
+    if (!m) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    cudaDeviceSynchronize();
+    cudaFree(m->d_fmeta);
+    cudaFree(m->d_borders);
+    cudaFree(m->d_chunks);
+    cudaFree(m->d_splits);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(m->d_stage[i]);
+        cudaFree(m->d_sstage[i]);
+        if (m->hs[i]) cudaStreamDestroy(m->hs[i]);
+        if (m->ev_out[i]) cudaEventDestroy(m->ev_out[i]);
+    }
+    if (m->ev_in) cudaEventDestroy(m->ev_in);
+    cudaSetDevice(prev);
+    delete m;
+}
+
+odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
+                          const float *leaf_values, int32_t depth, int64_t n_trees,
+                          int32_t n_features, int device, odf_model **out)
+{
+    if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (depth < 0 || depth > ODF_MAX_DEPTH) return fail(ODF_E_INVALID_ARG, "depth %d not in [0, %d]", depth, ODF_MAX_DEPTH);
+    if (n_trees < 0) return fail(ODF_E_INVALID_ARG, "n_trees < 0");
+    if (n_trees > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
+    if (n_features < 1) return fail(ODF_E_INVALID_ARG, "n_features < 1");
+    const int64_t n_nodes = n_trees * depth;
+    const int64_t n_leaves = n_trees << depth;
+    if (n_nodes > 0 && (!feature_index || !thresholds))
+        return fail(ODF_E_INVALID_ARG, "feature_index / thresholds is NULL");
+    if (n_leaves > 0 && !leaf_values) return fail(ODF_E_INVALID_ARG, "leaf_values is NULL");
+    for (int64_t k = 0; k < n_nodes; ++k) {
+        if (feature_index[k] < 0 || feature_index[k] >= n_features)
+            return fail(ODF_E_INVALID_ARG, "feature_index[%lld] = %d not in [0, n_features=%d)",
+                        (long long)k, feature_index[k], n_features);
+        if (!std::isfinite(thresholds[k]))
+            return fail(ODF_E_INVALID_ARG, "thresholds[%lld] is not finite", (long long)k);
+    }
+    for (int64_t k = 0; k < n_leaves; ++k)
+        if (!std::isfinite(leaf_values[k]))
+            return fail(ODF_E_INVALID_ARG, "leaf_values[%lld] is not finite", (long long)k);
+
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+        return fail(ODF_E_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    if (device < 0 || device >= n_dev) return fail(ODF_E_INVALID_ARG, "device %d not in [0, %d)", device, n_dev);
+
+    std::unique_ptr<odf_model> m(new odf_model());
+    m->device = device;
+    m->depth = depth;
+    m->n_trees = n_trees;
+    m->n_features = n_features;
+
+    // ---- borders per factor (sorted, unique by ==) ----
+    std::vector<std::vector<float>> borders(n_features);
+    for (int64_t k = 0; k < n_nodes; ++k) borders[feature_index[k]].push_back(thresholds[k]);
+    std::vector<int32_t> used_of(n_features, -1), colB_of(n_features, -1);
+    for (int32_t f = 0; f < n_features; ++f) {
+        auto &b = borders[f];
+        if (b.empty()) continue;
+        std::sort(b.begin(), b.end(), [](float a, float c) { return a < c; });
+        std::vector<float> u;
+        for (float v : b)
+            if (u.empty() || !(v == u.back())) u.push_back(v);
+        b.swap(u);
+        if (b.size() > ODF_MAX_BORDERS)
+            return fail(ODF_E_UNSUPPORTED, "factor %d has %zu distinct thresholds > %d (uint8 bins)",
+                        f, b.size(), ODF_MAX_BORDERS);
+        used_of[f] = static_cast<int32_t>(m->used_ids.size());
+        m->used_ids.push_back(f);
+        m->max_borders = std::max<int32_t>(m->max_borders, static_cast<int32_t>(b.size()));
+        m->total_borders += static_cast<int64_t>(b.size());
+    }
+    m->n_used = static_cast<int32_t>(m->used_ids.size());
+    std::vector<uint2> splits;
+    for (int32_t f : m->used_ids)
+        if (borders[f].size() > 127) {
+            colB_of[f] = m->n_used + static_cast<int32_t>(splits.size());
+            splits.push_back(make_uint2(static_cast<uint32_t>(used_of[f]) * kTile,
+                                        static_cast<uint32_t>(colB_of[f]) * kTile));
+        }
+    m->n_split = static_cast<int32_t>(splits.size());
+    m->n_cols = m->n_used + m->n_split;
+
+    // ---- factor metadata + padded, skewed border arrays (binarize) ----
+    m->n_fchunks = (n_features + kFSub - 1) / kFSub;
+    std::vector<uint4> fmeta(static_cast<size_t>(m->n_fchunks) * kFSub, make_uint4(0, 0, 0, kNoCol));
+    std::vector<float> bflat;
+    for (int32_t f : m->used_ids) {
+        const auto &b = borders[f];
+        const uint32_t mm = static_cast<uint32_t>(b.size());
+        uint32_t L = 0;
+        while (((1u << L) - 1u) < mm) ++L;  // 2^L - 1 >= m
+        const uint32_t n_pad = (1u << L) - 1u;
+        const uint32_t len = (n_pad - 1u) + ((n_pad - 1u) >> 5) + 1u;
+        const uint32_t off = static_cast<uint32_t>(bflat.size());
+        bflat.resize(bflat.size() + len, INFINITY);
+        for (uint32_t pidx = 0; pidx < n_pad; ++pidx)
+            bflat[off + pidx + (pidx >> 5)] = pidx < mm ? b[pidx] : INFINITY;
+        fmeta[f] = make_uint4(off, L | (mm << 8), static_cast<uint32_t>(used_of[f]) * kTile,
+                              colB_of[f] >= 0 ? static_cast<uint32_t>(colB_of[f]) * kTile : kNoCol);
+    }
+    while (bflat.size() % 4) bflat.push_back(INFINITY);
+    m->border_floats = static_cast<int32_t>(bflat.size());
+
+    // ---- tree chunks: descriptors + reversed leaf tables ----
+    const int dstride = ((depth + 1) & ~1) * 8;
+    m->table_stride = depth <= 6 ? 256u : (4u << depth);
+    const uint32_t per_tree = static_cast<uint32_t>(dstride) + m->table_stride;
+    m->tc = 16 * std::max<uint32_t>(1u, 20480u / (16u * per_tree));
+    m->desc_bytes = align_up(static_cast<uint64_t>(m->tc) * dstride, 256);
+    m->chunk_bytes = m->desc_bytes + static_cast<uint32_t>(m->tc) * m->table_stride;
+    m->n_tchunks = static_cast<int32_t>((n_trees + m->tc - 1) / m->tc);
+    std::vector<uint8_t> chunks(static_cast<size_t>(m->n_tchunks) * m->chunk_bytes, 0);
+    const uint32_t nleaf = 1u << depth;
+    for (int64_t t = 0; t < n_trees; ++t) {
+        uint8_t *ch = chunks.data() + static_cast<size_t>(t / m->tc) * m->chunk_bytes;
+        const int64_t i = t % m->tc;
+        uint32_t *desc = reinterpret_cast<uint32_t *>(ch + i * dstride);
+        for (int l = 0; l < depth; ++l) {
+            const int32_t f = feature_index[t * depth + l];
+            const float thr = thresholds[t * depth + l];
+            const auto &b = borders[f];
+            const auto it = std::lower_bound(b.begin(), b.end(), thr, [](float a, float c) { return a < c; });
+            const uint32_t k = static_cast<uint32_t>(it - b.begin());  // b[k] == thr
+            uint32_t col, K;
+            if (k + 1 <= 127) {
+                col = static_cast<uint32_t>(used_of[f]);
+                K = k + 1;
+            } else {
+                col = static_cast<uint32_t>(colB_of[f]);
+                K = k - 126;
+            }
+            desc[2 * l] = col * kTile;
+            desc[2 * l + 1] = (128u - K) * 0x01010101u;
+        }
+        float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
+        for (uint32_t F = 0; F < nleaf; ++F) tab[F] = leaf_values[t * nleaf + (nleaf - 1 - F)];
+    }
+
+    // ---- device ----
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&m->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
+        if (bytes == 0) return cudaSuccess;
+        cudaError_t r = cudaMalloc(dst, bytes);
+        if (r != cudaSuccess) return r;
+        m->dev_bytes += static_cast<int64_t>(bytes);
+        return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    };
+    if ((e = up(reinterpret_cast<void **>(&m->d_fmeta), fmeta.data(), fmeta.size() * sizeof(uint4))) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_borders), bflat.data(), bflat.size() * 4)) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_chunks), chunks.data(), chunks.size())) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_splits), splits.data(), splits.size() * sizeof(uint2))) != cudaSuccess) {
+        odf_model *raw = m.release();
+        odf_free_model(raw);
+        return e == cudaErrorMemoryAllocation ? fail(ODF_E_NOMEM, "device allocation failed")
+                                              : cuda_fail(e, "model upload");
+    }
+    if ((e = prepare_kernels(m->max_smem)) != cudaSuccess) {
+        odf_free_model(m.release());
+        return cuda_fail(e, "cudaFuncSetAttribute");
+    }
+    std::string why;
+    if (!make_plan(*m, MODE_FUSED, m->fused, why) || !make_plan(*m, MODE_APPLY, m->apply, why) ||
+        !make_plan(*m, MODE_BINARIZE, m->binz, why)) {
+        odf_free_model(m.release());
+        return fail(ODF_E_UNSUPPORTED, "%s", why.c_str());
+    }
+    m->binz.grid_per_sm = occupancy_main(MODE_BINARIZE, 0, m->binz.smem);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        odf_free_model(m.release());
+        return cuda_fail(e, "odf_load_model");
+    }
+    *out = m.release();
+    return ok();
+}
+
+odf_status odf_get_info(const odf_model *m, odf_model_info *info)
+{
+    if (!m || !info) return fail(ODF_E_INVALID_ARG, "NULL argument");
+    info->depth = m->depth;
+    info->n_features = m->n_features;
+    info->n_used_features = m->n_used;
+    info->n_split_features = m->n_split;
+    info->n_columns = m->n_cols;
+    info->n_trees = m->n_trees;
+    info->trees_per_chunk = m->tc;
+    info->n_tree_chunks = m->n_tchunks;
+    info->chunk_bytes = m->chunk_bytes;
+    info->model_device_bytes = m->dev_bytes;
+    info->max_borders = m->max_borders;
+    info->total_borders = m->total_borders;
+    info->borders_in_smem = m->fused.bsm ? 1 : 0;
+    info->stages_fused = m->fused.stages;
+    info->smem_fused = static_cast<int32_t>(m->fused.smem);
+    info->num_sms = m->num_sms;
+    return ok();
+}
+
+odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
+                           int32_t *n_used_features, const int32_t **used_feature_ids)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    const int64_t tiles = (n_docs + kTile - 1) / kTile;
+    if (bytes) *bytes = static_cast<size_t>(tiles) * m->n_used * kTile;
+    if (n_used_features) *n_used_features = m->n_used;
+    if (used_feature_ids) *used_feature_ids = m->used_ids.empty() ? nullptr : m->used_ids.data();
+    return ok();
+}
+
+static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64_t n_docs, int64_t ld,
+                           const uint8_t *bins_in, uint8_t *bins_out, float *scores, cudaStream_t s)
+{
+    const Plan &pl = mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
+    KParams p = base_params(m, pl);
+    p.n_docs = n_docs;
+    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.bins_in = bins_in;
+    p.bins_out = bins_out;
+    p.scores = scores;
+    CUtensorMap tm;
+    const CUtensorMap *tmp = nullptr;
+    if (mode != MODE_APPLY && p.n_fchunks > 0) {
+        odf_status st = encode_tmap(m, d_x, n_docs, ld, &tm);
+        if (st != ODF_OK) return st;
+        tmp = &tm;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != m->device) cudaSetDevice(m->device);
+    cudaError_t e = launch_main(mode, m->depth, p, tmp, grid_for(m, pl, p.n_tiles), pl.smem, s);
+    if (prev != m->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    return ok();
+}
+
+odf_status odf_binarize(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                        uint8_t *d_bins, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    odf_status st = check_factors(m, d_factors, n_docs, ld);
+    if (st != ODF_OK) return st;
+    if (n_docs == 0 || m->n_used == 0) return ok();
+    if (!d_bins) return fail(ODF_E_INVALID_ARG, "d_bins is NULL");
+    return run_main(m, MODE_BINARIZE, d_factors, n_docs, ld, nullptr, d_bins, nullptr,
+                    static_cast<cudaStream_t>(stream));
+}
+
+odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, float *d_scores,
+                     void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs == 0) return ok();
+    if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    if (m->n_used > 0 && !d_bins) return fail(ODF_E_INVALID_ARG, "d_bins is NULL");
+    if (reinterpret_cast<uintptr_t>(d_bins) % 16 != 0)
+        return fail(ODF_E_INVALID_ARG, "d_bins not 16-byte aligned");
+    return run_main(m, MODE_APPLY, nullptr, n_docs, 0, d_bins, nullptr, d_scores,
+                    static_cast<cudaStream_t>(stream));
+}
+
+odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                     float *d_scores, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    odf_status st = check_factors(m, d_factors, n_docs, ld);
+    if (st != ODF_OK) return st;
+    if (n_docs == 0) return ok();
+    if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, d_scores,
+                    static_cast<cudaStream_t>(stream));
+}
+
+static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, bool fp,
+                            int64_t doc0, int64_t ndoc, int64_t tree0, int64_t ntree,
+                            uint16_t *d_idx, uint64_t *d_fp, cudaStream_t s)
+{
+    KParams p = base_params(m, m->apply);
+    p.n_docs = n_docs;
+    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.bins_in = d_bins;
+    p.doc0 = doc0;
+    p.ndoc = ndoc;
+    p.tree0 = tree0;
+    p.ntree = ntree;
+    p.idx_out = d_idx;
+    p.fp_out = d_fp;
+    const int grid = fp ? static_cast<int>(p.n_tiles)
+                        : static_cast<int>((doc0 + ndoc - 1) / kTile - doc0 / kTile + 1);
+    const int dstride = ((m->depth + 1) & ~1) * 8;
+    const size_t smem = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
+                        align_up(static_cast<uint64_t>(m->tc) * dstride, 16) + 1024;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != m->device) cudaSetDevice(m->device);
+    cudaError_t e = launch_index(m->depth, p, fp, grid, smem, s);
+    if (prev != m->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "index kernel launch");
+    return ok();
+}
+
+odf_status odf_leaf_indices(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, int64_t doc0,
+                            int64_t ndoc, int64_t tree0, int64_t ntree, uint16_t *d_idx,
+                            void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (doc0 < 0 || ndoc < 0 || doc0 + ndoc > n_docs)
+        return fail(ODF_E_INVALID_ARG, "document window [%lld, %lld) outside [0, %lld)",
+                    (long long)doc0, (long long)(doc0 + ndoc), (long long)n_docs);
+    if (tree0 < 0 || ntree < 0 || tree0 + ntree > m->n_trees)
+        return fail(ODF_E_INVALID_ARG, "tree window [%lld, %lld) outside [0, %lld)",
+                    (long long)tree0, (long long)(tree0 + ntree), (long long)m->n_trees);
+    if (ndoc == 0 || ntree == 0) return ok();
+    if (!d_idx || (m->n_used > 0 && !d_bins)) return fail(ODF_E_INVALID_ARG, "NULL buffer");
+    return run_index(m, d_bins, n_docs, false, doc0, ndoc, tree0, ntree, d_idx, nullptr,
+                     static_cast<cudaStream_t>(stream));
+}
+
+odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                                 uint64_t *d_fp, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs == 0) return ok();
+    if (!d_fp || (m->n_used > 0 && !d_bins)) return fail(ODF_E_INVALID_ARG, "NULL buffer");
+    return run_index(m, d_bins, n_docs, true, 0, n_docs, 0, m->n_trees, nullptr, d_fp,
+                     static_cast<cudaStream_t>(stream));
+}
+
+odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,
+                          float *h_scores, int64_t chunk_docs, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (n_docs < 0 || ld < m->n_features || ld % 4 != 0)
+        return fail(ODF_E_INVALID_ARG, "bad n_docs / ld (ld >= n_features, ld %% 4 == 0)");
+    if (n_docs == 0) return ok();
+    if (!h_factors || !h_scores) return fail(ODF_E_INVALID_ARG, "NULL host buffer");
+    if (chunk_docs <= 0) chunk_docs = 65536;
+    chunk_docs = (chunk_docs + kTile - 1) / kTile * kTile;
+    std::lock_guard<std::mutex> lock(m->host_mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    cudaError_t e;
+    if (!m->hs[0] || m->stage_rows < chunk_docs || m->stage_ld < ld) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(m->d_stage[i]);
+            cudaFree(m->d_sstage[i]);
+            m->d_stage[i] = nullptr;
+            m->d_sstage[i] = nullptr;
+            if ((e = cudaMalloc(&m->d_stage[i], static_cast<size_t>(chunk_docs) * ld * 4)) != cudaSuccess ||
+                (e = cudaMalloc(&m->d_sstage[i], static_cast<size_t>(chunk_docs) * 4)) != cudaSuccess)
+                return fail(ODF_E_NOMEM, "staging allocation failed");
+            if (!m->hs[i]) cudaStreamCreateWithFlags(&m->hs[i], cudaStreamNonBlocking);
+            if (!m->ev_out[i]) cudaEventCreateWithFlags(&m->ev_out[i], cudaEventDisableTiming);
+        }
+        if (!m->ev_in) cudaEventCreateWithFlags(&m->ev_in, cudaEventDisableTiming);
+        m->stage_rows = chunk_docs;
+        m->stage_ld = ld;
+    }
+    cudaStream_t us = static_cast<cudaStream_t>(stream);
+    cudaEventRecord(m->ev_in, us);
+    cudaStreamWaitEvent(m->hs[0], m->ev_in, 0);
+    cudaStreamWaitEvent(m->hs[1], m->ev_in, 0);
+    int64_t k = 0;
+    for (int64_t d0 = 0; d0 < n_docs; d0 += chunk_docs, ++k) {
+        const int b = static_cast<int>(k & 1);
+        const int64_t n = std::min<int64_t>(chunk_docs, n_docs - d0);
+        cudaStream_t s = m->hs[b];
+        if ((e = cudaMemcpyAsync(m->d_stage[b], h_factors + d0 * ld, static_cast<size_t>(n) * ld * 4,
+                                 cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e, "H2D");
+        odf_status st = odf_score(m, m->d_stage[b], n, ld, m->d_sstage[b], s);
+        if (st != ODF_OK) return st;
+        if ((e = cudaMemcpyAsync(h_scores + d0, m->d_sstage[b], static_cast<size_t>(n) * 4,
+                                 cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+            return cuda_fail(e, "D2H");
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaEventRecord(m->ev_out[i], m->hs[i]);
+        cudaStreamWaitEvent(us, m->ev_out[i], 0);
+    }
+    if ((e = cudaStreamSynchronize(us)) != cudaSuccess) return cuda_fail(e, "odf_score_host");
+    return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,664 @@
+// odf_kernels.cu -- sm_100a kernels of the oblivious-forest hot path.
+//
+//   K1 binarize   fp32 factors (TMA-staged, 128B-swizzled tiles) -> uint8 bins
+//   K2 apply      bins -> per-document fp32 scores
+//   K3 fused      K1 o K2 per 128-document tile; bins live only in shared memory
+//   K6 index      leaf-index export / per-document FNV-1a fingerprint (tests)
+//
+// Paper: arxiv 2205.07307.  Node condition FACTOR[INDEX] < THRESHOLD
+// (P:80); leaf index = the level conditions written as a binary number, true = 1
+// (P:114-116), level l = bit l; score = sum over trees.  The
+// binarized form is the north_star's uint8 bin = #{borders <= x}.
+//
+// One CTA = 16 consumer warps + 1 producer warp, persistent over 128-document
+// tiles.  The producer streams, through one ring of shared-memory slots guarded
+// by mbarriers, first the tile's factor sub-tiles (cp.async.bulk.tensor, TMA)
+// and then the forest's tree chunks (cp.async.bulk), so the next tile's HBM
+// reads start while the current tile's trees are still being applied.
+//
+// Exactness: every comparison is IEEE fp32 (no fast-math, no FTZ); index
+// assembly is integer-exact; the fp32 summation order is fixed (DESIGN.md
+// "Summation order"): group g = t mod 16 sums its trees in ascending order, and
+// score = (((P_0 + P_1) + P_2) + ... + P_15).  Every kernel here uses that order.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "odf_internal.h"
+
+namespace odf {
+
+// ---------------------------------------------------------------------------
+// PTX helpers (shared-window 32-bit addresses throughout)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds_v2u(uint32_t a)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_v4u(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_v4f(uint32_t a)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v)
+{
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4f(uint32_t a, float x, float y, float z, float w)
+{
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z),
+                 "f"(w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts_v4u(uint32_t a, uint4 v)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
+{
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+__device__ __forceinline__ void named_bar_consumers()
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerThreads) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "ODF_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra ODF_WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all()
+{
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all()
+{
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1: binarization of one 128-doc x 32-factor sub-tile
+// ---------------------------------------------------------------------------
+// The TMA box lands with SWIZZLE_128B: 16-byte chunk q of row r sits at chunk
+// q ^ (r & 7), so the LDS.128 of a warp (32 rows, one chunk) is conflict-free.
+// Warp w handles documents (w&3)*32 + lane and factor quads (w>>2), (w>>2)+4.
+// bin(x) = #{j : !(x < b_j)} by a branchless search over the factor's sorted
+// borders padded to 2^L - 1 entries with +inf (the predicate !(x < b) is a
+// prefix of the sorted array for every x, NaN and +inf included; the result is
+// then clamped to m).  The 4 searches of a quad run interleaved.
+template <bool CODES, bool BSMEM>
+__device__ __forceinline__ void binarize_sub(uint32_t stage, int fchunk, const KParams &p,
+                                             uint32_t bins, uint32_t bsm, int warp, int lane)
+{
+    const int doc = ((warp & 3) << 5) | lane;
+    const uint32_t row = stage + doc * 128;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int q = (warp >> 2) + 4 * h;
+        const int f0 = fchunk * kFSub + q * 4;
+        uint4 m[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[j] = __ldg(p.fmeta + f0 + j);
+        int L[4];
+        int lmax = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            L[j] = static_cast<int>(m[j].y & 0xffu);
+            lmax = max(lmax, L[j]);
+        }
+        if (lmax == 0) continue;  // warp-uniform: no used factor in this quad
+        const float4 v = lds_v4f(row + ((q ^ (doc & 7)) << 4));
+        const float x[4] = {v.x, v.y, v.z, v.w};
+        uint32_t pos[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pos[j] = m[j].x * 4u;
+        for (int st = lmax - 1; st >= 0; --st) {
+            const uint32_t s = 1u << st;
+            const uint32_t off = 4u * ((s - 1) + ((s - 1) >> 5));  // skewed position of s-1
+            const uint32_t inc = 4u * (s + (s >> 5));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (L[j] > st) {
+                    float b;
+                    if (BSMEM)
+                        b = lds_f32(bsm + pos[j] + off);
+                    else
+                        b = __ldg(reinterpret_cast<const float *>(
+                            reinterpret_cast<const char *>(p.borders) + pos[j] + off));
+                    if (!(x[j] < b)) pos[j] += inc;  // condition false -> border counted
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (L[j] == 0) continue;
+            const uint32_t ip = (pos[j] - m[j].x * 4u) >> 2;  // skewed index
+            const uint32_t idx = ip - ip / 33u;                // unskew (idx < 1056)
+            const uint32_t bin = min(idx, m[j].y >> 8);
+            if (CODES) {
+                sts_u8(bins + m[j].z + doc, min(bin, 127u));
+                if (m[j].w != kNoCol) sts_u8(bins + m[j].w + doc, bin > 127u ? bin - 127u : 0u);
+            } else {
+                sts_u8(bins + m[j].z + doc, bin);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2: leaf-index assembly (SWAR, 4 documents per lane)
+// ---------------------------------------------------------------------------
+// Lane j holds documents 4j..4j+3 of the tile as the 4 bytes of one u32 read
+// from the bins row of a column.  Codes are 7-bit (factors with > 127 borders
+// use two columns), so for a level with descriptor
+// {col*128, (128-K)*0x01010101} the byte sum code + 128 - K never carries out
+// of its byte and its bit 7 is the "flag" code >= K, i.e. the condition is
+// FALSE.  Flags are shifted in from the top of each byte, so after DEPTH levels
+// level l sits at bit 8-DEPTH+l: the byte is the complemented leaf index F,
+// and leaf tables are stored reversed (table[F] = leaf[2^d-1-F]).
+template <int DEPTH>
+__device__ __forceinline__ void tree_level(uint32_t col, uint32_t add, uint32_t lane_bins, int l,
+                                           uint32_t &lo, uint32_t &hi)
+{
+    const uint32_t w = lds_u32(col + lane_bins);
+    const uint32_t s = (w + add) & 0x80808080u;
+    if (l < 8)
+        lo = (l == 0) ? s : ((lo >> 1) | s);
+    else
+        hi = (l == 8) ? s : ((hi >> 1) | s);
+}
+
+template <int DEPTH>
+__device__ __forceinline__ void tree_flags(uint32_t d, uint32_t lane_bins, uint32_t &lo,
+                                           uint32_t &hi)
+{
+    lo = 0;
+    hi = 0;
+#pragma unroll
+    for (int l = 0; l < DEPTH; l += 2) {
+        if (l + 1 < DEPTH) {
+            const uint4 q = lds_v4u(d + l * 8);
+            tree_level<DEPTH>(q.x, q.y, lane_bins, l, lo, hi);
+            tree_level<DEPTH>(q.z, q.w, lane_bins, l + 1, lo, hi);
+        } else {
+            const uint2 q = lds_v2u(d + l * 8);
+            tree_level<DEPTH>(q.x, q.y, lane_bins, l, lo, hi);
+        }
+    }
+}
+
+// Complemented leaf index F of the lane's 4 documents.
+template <int DEPTH>
+__device__ __forceinline__ void tree_findex(uint32_t d, uint32_t lane_bins, uint32_t F[4])
+{
+    uint32_t lo, hi;
+    tree_flags<DEPTH>(d, lane_bins, lo, hi);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+        if constexpr (DEPTH == 0) {
+            F[n] = 0;
+        } else if constexpr (DEPTH <= 8) {
+            F[n] = ((lo >> (8 * n)) & 0xffu) >> (8 - DEPTH);
+        } else {
+            const uint32_t h = hi >> (16 - DEPTH);
+            F[n] = ((lo >> (8 * n)) & 0xffu) | (((h >> (8 * n)) & 0xffu) << 8);
+        }
+    }
+}
+
+// Shared-memory addresses of the 4 leaves (tables reversed; table base tb).
+template <int DEPTH>
+__device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint32_t tb,
+                                           uint32_t a[4])
+{
+    uint32_t lo, hi;
+    tree_flags<DEPTH>(d, lane_bins, lo, hi);
+    if constexpr (DEPTH <= 6) {
+        // byte = F << (8-DEPTH); want 4F in the low byte of a 256-aligned base
+        if constexpr (DEPTH < 6 && DEPTH > 0) lo >>= (6 - DEPTH);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) a[n] = prmt(lo, tb, 0x7650u | n);
+    } else if constexpr (DEPTH <= 8) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) a[n] = tb + (prmt(lo, 0u, 0x4440u | n) << (DEPTH - 6));
+    } else {
+        const uint32_t h = hi >> (16 - DEPTH);
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+            a[n] = tb + (prmt(lo, h, 0xCC00u | ((4u + n) << 4) | n) << 2);
+    }
+}
+
+__host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 1) & ~1) * 8; }
+
+template <int DEPTH>
+__device__ __forceinline__ void apply_chunk(uint32_t chunk, int n_in, uint32_t desc_bytes,
+                                            uint32_t stride, uint32_t lane_bins, int warp,
+                                            float acc[4])
+{
+#pragma unroll 2
+    for (int i = warp; i < n_in; i += kConsumerWarps) {
+        const uint32_t d = chunk + i * desc_stride(DEPTH);
+        const uint32_t tb = chunk + desc_bytes + i * stride;
+        uint32_t a[4];
+        leaf_addrs<DEPTH>(d, lane_bins, tb, a);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) acc[n] += lds_f32(a[n]);
+    }
+}
+
+// Split factors (> 127 borders) loaded as true bins: column A <- min(bin,127),
+// column B <- max(bin-127, 0).
+__device__ __forceinline__ void expand_splits(const KParams &p, uint32_t bins, int tid, int nthr)
+{
+    for (int k = tid; k < p.n_split * (kTile / 4); k += nthr) {
+        const uint2 sp = p.splits[k / (kTile / 4)];
+        const uint32_t wd = (k % (kTile / 4)) * 4;
+        const uint32_t w = lds_u32(bins + sp.x + wd);
+        sts_u32(bins + sp.x + wd, __vminu4(w, 0x7f7f7f7fu));
+        sts_u32(bins + sp.y + wd, __vsubus4(w, 0x7f7f7f7fu));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Main persistent kernel: MODE_FUSED (K3), MODE_BINARIZE (K1), MODE_APPLY (K2)
+// ---------------------------------------------------------------------------
+template <int MODE, int DEPTH, bool BSMEM>
+__global__ void __launch_bounds__(kThreads, 1)
+    odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ uint8_t smem_raw[];
+    constexpr bool HAS_A = MODE != MODE_APPLY;
+    constexpr bool HAS_B = MODE != MODE_BINARIZE;
+    const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    const uint32_t bins = base + p.off_bins;
+    const uint32_t ring = base + p.off_ring;
+    const uint32_t red = base + p.off_red;
+    const uint32_t bars = base + p.off_bars;
+    const uint32_t bsm = base + p.off_borders;
+    const int S = p.stages;
+    const uint32_t bins_full = bars + 16u * S, bins_empty = bins_full + 8u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_fjobs = HAS_A ? (p.n_fchunks + p.fsub_per_job - 1) / p.fsub_per_job : 0;
+    const int n_bjobs = HAS_B ? p.n_tchunks : 0;
+    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(bars + 16u * s, 1);                   // full[s]: producer + tx bytes
+            mbar_init(bars + 16u * s + 8u, kConsumerWarps);  // empty[s]: one arrive per warp
+        }
+        mbar_init(bins_full, 1);
+        mbar_init(bins_empty, kConsumerWarps);
+        fence_barrier_init();
+    }
+    if (BSMEM) {
+        for (int i = threadIdx.x; i < p.border_floats; i += kThreads)
+            sts_f32(bsm + 4u * i, __ldg(p.borders + i));
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ===================== producer warp (one elected lane) =====================
+        if (lane == 0) {
+            if (HAS_A && n_fjobs > 0)
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap))
+                             : "memory");
+            uint32_t slot = 0, ph = 0, bph = 0;
+            for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+                if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
+                    mbar_wait(bins_empty, bph ^ 1u);
+                    mbar_expect_tx(bins_full, tile_bins_bytes);
+                    bulk_g2s(bins, p.bins_in + tile * tile_bins_bytes, tile_bins_bytes, bins_full);
+                    bph ^= 1u;
+                }
+                for (int j = 0; j < n_fjobs; ++j) {
+                    const uint32_t full = bars + 16u * slot, empty = full + 8u;
+                    mbar_wait(empty, ph ^ 1u);
+                    const int c0 = j * p.fsub_per_job;
+                    const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
+                    mbar_expect_tx(full, nsub * kFSubBytes);
+                    for (int s = 0; s < nsub; ++s)
+                        tma_load_2d(ring + slot * p.slot_bytes + s * kFSubBytes, &tmap,
+                                    (c0 + s) * kFSub, static_cast<int>(tile * kTile), full);
+                    if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+                }
+                for (int c = 0; c < n_bjobs; ++c) {
+                    const uint32_t full = bars + 16u * slot, empty = full + 8u;
+                    mbar_wait(empty, ph ^ 1u);
+                    mbar_expect_tx(full, p.chunk_bytes);
+                    bulk_g2s(ring + slot * p.slot_bytes,
+                             p.chunks + static_cast<size_t>(c) * p.chunk_bytes, p.chunk_bytes, full);
+                    if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+                }
+            }
+        }
+        return;
+    }
+
+    // ========================= consumer warps =========================
+    const int tid = threadIdx.x;
+    const uint32_t lane_bins = bins + lane * 4u;
+    uint32_t slot = 0, ph = 0, bph = 0;
+    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        if (MODE == MODE_BINARIZE && tile != blockIdx.x) {
+            if (tid == 0) bulk_wait_read_all();  // previous tile's bins fully read by TMA store
+            named_bar_consumers();
+        }
+        if (HAS_A) {
+            for (int j = 0; j < n_fjobs; ++j) {
+                const uint32_t full = bars + 16u * slot, empty = full + 8u;
+                mbar_wait(full, ph);
+                const int c0 = j * p.fsub_per_job;
+                const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
+                for (int s = 0; s < nsub; ++s)
+                    binarize_sub<MODE == MODE_FUSED, BSMEM>(ring + slot * p.slot_bytes + s * kFSubBytes,
+                                                            c0 + s, p, bins, bsm, warp, lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty);
+                if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+            }
+        }
+        if (MODE == MODE_BINARIZE) {
+            fence_proxy_async();  // generic-proxy bin stores -> visible to the TMA store
+            named_bar_consumers();
+            if (tid == 0 && tile_bins_bytes > 0)
+                bulk_s2g(p.bins_out + tile * tile_bins_bytes, bins, tile_bins_bytes);
+            continue;
+        }
+        if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
+            mbar_wait(bins_full, bph);
+            bph ^= 1u;
+            expand_splits(p, bins, tid, kConsumerThreads);
+        }
+        named_bar_consumers();  // all bins of the tile written
+
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < n_bjobs; ++c) {
+            const uint32_t full = bars + 16u * slot, empty = full + 8u;
+            mbar_wait(full, ph);
+            const int64_t rem = p.n_trees - static_cast<int64_t>(c) * p.tc;
+            const int n_in = rem < p.tc ? static_cast<int>(rem) : p.tc;
+            apply_chunk<DEPTH>(ring + slot * p.slot_bytes, n_in, p.desc_bytes, p.table_stride,
+                               lane_bins, warp, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty);
+            if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+        }
+        if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
+            fence_proxy_async();  // expand_splits wrote bins; the next TMA overwrites them
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bins_empty);
+        }
+        sts_v4f(red + warp * (kTile * 4) + lane * 16, acc[0], acc[1], acc[2], acc[3]);
+        named_bar_consumers();
+        if (tid < kTile) {
+            float s = lds_f32(red + tid * 4);
+#pragma unroll
+            for (int w = 1; w < kConsumerWarps; ++w) s += lds_f32(red + w * (kTile * 4) + tid * 4);
+            const int64_t doc = tile * kTile + tid;
+            if (doc < p.n_docs) p.scores[doc] = s;
+        }
+        named_bar_consumers();
+    }
+    if (MODE == MODE_BINARIZE && tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// K6: leaf-index export and per-document fingerprint (tests).  Same tree_flags
+// as the apply path; bins and descriptors staged in shared memory by plain loads.
+// ---------------------------------------------------------------------------
+template <int DEPTH>
+__global__ void __launch_bounds__(kConsumerThreads)
+    odf_index_kernel(const KParams p, int fingerprint)
+{
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    const uint32_t bins = base;
+    const uint32_t descs = base + ((static_cast<uint32_t>(p.n_cols) * kTile + 1023u) & ~1023u);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile;
+    const int64_t tile = (fingerprint ? 0 : p.doc0 / kTile) + blockIdx.x;
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.bins_in + tile * tile_bins_bytes);
+        for (uint32_t k = tid; k < tile_bins_bytes / 16; k += kConsumerThreads)
+            sts_v4u(bins + 16 * k, __ldg(src + k));
+        __syncthreads();
+        expand_splits(p, bins, tid, kConsumerThreads);
+        __syncthreads();
+    }
+    const uint32_t lane_bins = bins + lane * 4u;
+    const int64_t t_lo = fingerprint ? 0 : p.tree0;
+    const int64_t t_hi = fingerprint ? p.n_trees : p.tree0 + p.ntree;
+    uint64_t h[4] = {0xcbf29ce484222325ull, 0xcbf29ce484222325ull, 0xcbf29ce484222325ull,
+                     0xcbf29ce484222325ull};
+    for (int64_t c = t_lo / p.tc; c * p.tc < t_hi; ++c) {
+        const uint8_t *chunk = p.chunks + static_cast<size_t>(c) * p.chunk_bytes;
+        const uint32_t dbytes = static_cast<uint32_t>(p.tc) * desc_stride(DEPTH);
+        for (uint32_t k = tid; k < dbytes / 16; k += kConsumerThreads)
+            sts_v4u(descs + 16 * k, __ldg(reinterpret_cast<const uint4 *>(chunk) + k));
+        __syncthreads();
+        const int64_t c0 = c * p.tc;
+        if (fingerprint) {
+            if (warp == 0) {
+                for (int i = 0; i < p.tc && c0 + i < p.n_trees; ++i) {
+                    uint32_t F[4];
+                    tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), lane_bins, F);
+#pragma unroll
+                    for (int n = 0; n < 4; ++n) {
+                        const uint32_t idx = F[n] ^ ((1u << DEPTH) - 1u);
+                        h[n] = (h[n] ^ (idx & 0xffu)) * 0x100000001b3ull;
+                        h[n] = (h[n] ^ (idx >> 8)) * 0x100000001b3ull;
+                    }
+                }
+            }
+        } else {
+            for (int i = warp; i < p.tc; i += kConsumerWarps) {
+                const int64_t t = c0 + i;
+                if (t < p.tree0 || t >= t_hi) continue;
+                uint32_t F[4];
+                tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), lane_bins, F);
+#pragma unroll
+                for (int n = 0; n < 4; ++n) {
+                    const int64_t doc = tile * kTile + lane * 4 + n;
+                    if (doc >= p.doc0 && doc < p.doc0 + p.ndoc)
+                        p.idx_out[(doc - p.doc0) * p.ntree + (t - p.tree0)] =
+                            static_cast<uint16_t>(F[n] ^ ((1u << DEPTH) - 1u));
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (fingerprint && warp == 0) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const int64_t doc = tile * kTile + lane * 4 + n;
+            if (doc < p.n_docs) p.fp_out[doc] = h[n];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+template <int MODE, int DEPTH, bool BSMEM>
+static const void *main_fn()
+{
+    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH, BSMEM>);
+}
+
+#define ODF_DEPTH_TABLE(M, B)                                                              \
+    {main_fn<M, 0, B>(), main_fn<M, 1, B>(), main_fn<M, 2, B>(), main_fn<M, 3, B>(),       \
+     main_fn<M, 4, B>(), main_fn<M, 5, B>(), main_fn<M, 6, B>(), main_fn<M, 7, B>(),       \
+     main_fn<M, 8, B>(), main_fn<M, 9, B>(), main_fn<M, 10, B>()}
+
+static const void *main_kernel(int mode, int depth, bool bsmem)
+{
+    static const void *fused[2][11] = {ODF_DEPTH_TABLE(MODE_FUSED, false),
+                                       ODF_DEPTH_TABLE(MODE_FUSED, true)};
+    static const void *apply[11] = ODF_DEPTH_TABLE(MODE_APPLY, false);
+    static const void *binz[2] = {main_fn<MODE_BINARIZE, 0, false>(),
+                                  main_fn<MODE_BINARIZE, 0, true>()};
+    if (depth < 0 || depth > 10) return nullptr;
+    if (mode == MODE_FUSED) return fused[bsmem ? 1 : 0][depth];
+    if (mode == MODE_APPLY) return apply[depth];
+    return binz[bsmem ? 1 : 0];
+}
+
+template <int DEPTH>
+static const void *index_fn()
+{
+    return reinterpret_cast<const void *>(&odf_index_kernel<DEPTH>);
+}
+static const void *index_kernel(int depth)
+{
+    static const void *t[11] = {index_fn<0>(), index_fn<1>(), index_fn<2>(), index_fn<3>(),
+                                index_fn<4>(), index_fn<5>(), index_fn<6>(), index_fn<7>(),
+                                index_fn<8>(), index_fn<9>(), index_fn<10>()};
+    return (depth < 0 || depth > 10) ? nullptr : t[depth];
+}
+
+cudaError_t prepare_kernels(int max_smem)
+{
+    for (int d = 0; d <= 10; ++d) {
+        const void *fs[] = {main_kernel(MODE_FUSED, d, false), main_kernel(MODE_FUSED, d, true),
+                            main_kernel(MODE_APPLY, d, false), index_kernel(d)};
+        for (const void *f : fs) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = cudaFuncSetAttribute(main_kernel(MODE_BINARIZE, 0, b != 0),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+int occupancy_main(int mode, int depth, size_t smem)
+{
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, main_kernel(mode, depth, false), kThreads,
+                                                      smem) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
+                        size_t smem, cudaStream_t s)
+{
+    const void *f = main_kernel(mode, depth, p.borders_smem != 0);
+    if (!f) return cudaErrorInvalidValue;
+    KParams pc = p;
+    CUtensorMap tm;
+    if (tmap)
+        tm = *tmap;
+    else
+        memset(&tm, 0, sizeof(tm));
+    void *args[] = {&pc, &tm};
+    return cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, s);
+}
+
+cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
+                         cudaStream_t s)
+{
+    const void *f = index_kernel(depth);
+    if (!f) return cudaErrorInvalidValue;
+    KParams pc = p;
+    int fp = fingerprint ? 1 : 0;
+    void *args[] = {&pc, &fp};
+    return cudaLaunchKernel(f, dim3(grid), dim3(kConsumerThreads), args, smem, s);
+}
+
+}  // namespace odf

@@ -1,0 +1,245 @@
+"""Thin Python binding of the C ABI in include/odf.h (argument marshalling only).
+
+Every step of the hot path runs in libodf.so's CUDA kernels; this module only
+passes torch tensors' device pointers, sizes and the current CUDA stream.  If
+the library is missing or fails to load, importing the binding raises: there is
+no CPU fallback.  torch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import build as _build
+
+TILE_DOCS = 128
+MAX_DEPTH = 10
+MAX_BORDERS = 254
+
+_STATUS = {0: "ODF_OK", 1: "ODF_E_INVALID_ARG", 2: "ODF_E_UNSUPPORTED", 3: "ODF_E_NOMEM",
+           4: "ODF_E_CUDA"}
+
+
+class OdfError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("depth", ctypes.c_int32), ("n_features", ctypes.c_int32),
+                ("n_used_features", ctypes.c_int32), ("n_split_features", ctypes.c_int32),
+                ("n_columns", ctypes.c_int32), ("n_trees", ctypes.c_int64),
+                ("trees_per_chunk", ctypes.c_int32), ("n_tree_chunks", ctypes.c_int32),
+                ("chunk_bytes", ctypes.c_int64), ("model_device_bytes", ctypes.c_int64),
+                ("max_borders", ctypes.c_int32), ("total_borders", ctypes.c_int64),
+                ("borders_in_smem", ctypes.c_int32), ("stages_fused", ctypes.c_int32),
+                ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32)]
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Load libodf.so (building it first if the sources are newer).  Raises if it cannot."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if _build._stale():
+        try:
+            _build.build()
+        except Exception as e:  # no silent fallback: the CUDA path is the product
+            if not os.path.exists(path):
+                raise RuntimeError(f"libodf.so is missing and could not be built: {e}") from e
+    L = ctypes.CDLL(path)
+    L.odf_version.restype = ctypes.c_int
+    L.odf_last_error.restype = ctypes.c_char_p
+    L.odf_load_model.restype = ctypes.c_int
+    L.odf_load_model.argtypes = [_vp, _vp, _vp, _i32, _i64, _i32, ctypes.c_int,
+                                 ctypes.POINTER(_vp)]
+    L.odf_free_model.restype = None
+    L.odf_free_model.argtypes = [_vp]
+    L.odf_get_info.restype = ctypes.c_int
+    L.odf_get_info.argtypes = [_vp, ctypes.POINTER(_Info)]
+    L.odf_bins_layout.restype = ctypes.c_int
+    L.odf_bins_layout.argtypes = [_vp, _i64, ctypes.POINTER(ctypes.c_size_t),
+                                  ctypes.POINTER(_i32), ctypes.POINTER(ctypes.POINTER(_i32))]
+    L.odf_binarize.restype = ctypes.c_int
+    L.odf_binarize.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+    L.odf_apply.restype = ctypes.c_int
+    L.odf_apply.argtypes = [_vp, _vp, _i64, _vp, _vp]
+    L.odf_score.restype = ctypes.c_int
+    L.odf_score.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+    L.odf_leaf_indices.restype = ctypes.c_int
+    L.odf_leaf_indices.argtypes = [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]
+    L.odf_index_fingerprint.restype = ctypes.c_int
+    L.odf_index_fingerprint.argtypes = [_vp, _vp, _i64, _vp, _vp]
+    L.odf_score_host.restype = ctypes.c_int
+    L.odf_score_host.argtypes = [_vp, _vp, _i64, _i64, _vp, _i64, _vp]
+    _lib = L
+    return L
+
+
+ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_model",
+               "odf_get_info", "odf_bins_layout", "odf_binarize", "odf_apply", "odf_score",
+               "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host")
+
+
+def _check(status: int):
+    if status != 0:
+        raise OdfError(status, lib().odf_last_error().decode())
+
+
+def _stream(stream, device):
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return _vp(stream.cuda_stream)
+
+
+def _ptr(t):
+    return _vp(t.data_ptr()) if t is not None and t.numel() > 0 else _vp(0)
+
+
+def bins_to_canonical(bins: torch.Tensor, n_docs: int, n_used: int) -> torch.Tensor:
+    """Blocked layout [tile][used][128] -> [n_docs][n_used] (a view + copy, no arithmetic)."""
+    tiles = (n_docs + TILE_DOCS - 1) // TILE_DOCS
+    b = bins[: tiles * n_used * TILE_DOCS].view(tiles, n_used, TILE_DOCS)
+    return b.permute(0, 2, 1).reshape(tiles * TILE_DOCS, n_used)[:n_docs]
+
+
+class Model:
+    """An oblivious forest loaded onto one GPU (odf_load_model)."""
+
+    def __init__(self, feature_index, thresholds, leaf_values, depth: int, n_features: int,
+                 device: int = 0):
+        L = lib()
+        fi = np.ascontiguousarray(feature_index, dtype=np.int32)
+        thr = np.ascontiguousarray(thresholds, dtype=np.float32)
+        lv = np.ascontiguousarray(leaf_values, dtype=np.float32)
+        depth = int(depth)
+        n_trees = lv.size >> depth if depth >= 0 else 0
+        if depth >= 0 and (fi.size != n_trees * depth or thr.size != n_trees * depth
+                           or lv.size != n_trees << depth):
+            raise OdfError(1, f"array sizes {fi.size}/{thr.size}/{lv.size} inconsistent with "
+                              f"depth {depth}")
+        h = _vp()
+        _check(L.odf_load_model(fi.ctypes.data if fi.size else None,
+                                thr.ctypes.data if thr.size else None,
+                                lv.ctypes.data if lv.size else None,
+                                depth, n_trees, int(n_features), int(device), ctypes.byref(h)))
+        self._h = h
+        self.device = int(device)
+        self.depth = depth
+        self.n_trees = int(n_trees)
+        self.n_features = int(n_features)
+        inf = _Info()
+        _check(L.odf_get_info(self._h, ctypes.byref(inf)))
+        self.info = {k: getattr(inf, k) for k, _ in _Info._fields_}
+        n = _i32()
+        ids = ctypes.POINTER(_i32)()
+        nb = ctypes.c_size_t()
+        _check(L.odf_bins_layout(self._h, 0, ctypes.byref(nb), ctypes.byref(n), ctypes.byref(ids)))
+        self.n_used = int(n.value)
+        self.used_feature_ids = np.array([ids[i] for i in range(self.n_used)], np.int32)
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().odf_free_model(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- helpers ----------------------------------------------------------
+    def _dev(self):
+        return torch.device("cuda", self.device)
+
+    def bins_bytes(self, n_docs: int) -> int:
+        nb = ctypes.c_size_t()
+        _check(lib().odf_bins_layout(self._h, int(n_docs), ctypes.byref(nb), None, None))
+        return int(nb.value)
+
+    def _check_x(self, x: torch.Tensor):
+        if not (x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 and x.stride(1) == 1):
+            raise OdfError(1, "factors must be a CUDA float32 [n_docs, ld] tensor with unit "
+                              "column stride")
+        return x.shape[0], x.stride(0)
+
+    # -- hot path ---------------------------------------------------------
+    def binarize(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        n, ld = self._check_x(x)
+        if out is None:
+            out = torch.empty(self.bins_bytes(n), dtype=torch.uint8, device=self._dev())
+        _check(lib().odf_binarize(self._h, _ptr(x), n, ld, _ptr(out), _stream(stream, self._dev())))
+        return out
+
+    def apply(self, bins: torch.Tensor, n_docs: int, out: torch.Tensor | None = None, stream=None):
+        if out is None:
+            out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
+        _check(lib().odf_apply(self._h, _ptr(bins), int(n_docs), _ptr(out),
+                               _stream(stream, self._dev())))
+        return out
+
+    def score(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        n, ld = self._check_x(x)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self._dev())
+        _check(lib().odf_score(self._h, _ptr(x), n, ld, _ptr(out), _stream(stream, self._dev())))
+        return out
+
+    def score_host(self, x, out=None, chunk_docs: int = 65536, stream=None):
+        """End-to-end from host memory (numpy array or CPU tensor, ideally pinned)."""
+        if isinstance(x, torch.Tensor):
+            assert x.device.type == "cpu" and x.dtype == torch.float32 and x.stride(1) == 1
+            n, ld, xp = x.shape[0], x.stride(0), x.data_ptr()
+            if out is None:
+                out = torch.empty(n, dtype=torch.float32, pin_memory=x.is_pinned())
+            op = out.data_ptr()
+        else:
+            x = np.ascontiguousarray(x, dtype=np.float32)
+            n, ld, xp = x.shape[0], x.shape[1], x.ctypes.data
+            if out is None:
+                out = np.empty(n, np.float32)
+            op = out.ctypes.data
+        _check(lib().odf_score_host(self._h, _vp(xp), n, ld, _vp(op), int(chunk_docs),
+                                    _stream(stream, self._dev())))
+        return out
+
+    # -- test / debug (K6) ----------------------------------------------------
+    def leaf_indices(self, bins, n_docs, doc0, ndoc, tree0, ntree, stream=None):
+        out = torch.empty((int(ndoc), int(ntree)), dtype=torch.int16, device=self._dev())
+        _check(lib().odf_leaf_indices(self._h, _ptr(bins), int(n_docs), int(doc0), int(ndoc),
+                                      int(tree0), int(ntree), _ptr(out),
+                                      _stream(stream, self._dev())))
+        return out
+
+    def index_fingerprint(self, bins, n_docs, stream=None):
+        out = torch.empty(int(n_docs), dtype=torch.int64, device=self._dev())
+        _check(lib().odf_index_fingerprint(self._h, _ptr(bins), int(n_docs), _ptr(out),
+                                           _stream(stream, self._dev())))
+        return out
+
+    def canonical_bins(self, bins: torch.Tensor, n_docs: int) -> torch.Tensor:
+        return bins_to_canonical(bins, n_docs, self.n_used)

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs.
+
+Bar (BASELINE.json north_star):
+  * bins and leaf indices bit-exact (window export + per-document FNV fingerprint);
+  * scores |s_gpu - s_oracle64| <= 1e-5 * sum_t max_j |L_t[j]|;
+  * exact-arithmetic leaves (integer * 2^-20) -> scores bit-exact;
+  * fused odf_score == odf_binarize + odf_apply bit-for-bit (same summation order);
+  * a document's score does not depend on the batch it is scored in (bit-exact).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from helpers import cuda_model, oracle_bins_used, run_cuda, to_dev, tolerance
+
+pytestmark = pytest.mark.gpu
+
+SPEC_DOC_COUNTS = [1, 7, 16, 100, 127, 128, 129, 257, 1000, 1024]
+
+
+def _ld(f):
+    return (f + 3) // 4 * 4
+
+
+def full_check(case, check_fp=True, exact=False, idx_window=None):
+    import torch
+    n = case.n_docs
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    bins, s_fused, s_two = run_cuda(m, x, n)
+    # bins bit-exact
+    want_bins, used, _ = oracle_bins_used(case)
+    assert np.array_equal(m.used_feature_ids, used)
+    got_bins = m.canonical_bins(bins, n).cpu().numpy()
+    assert np.array_equal(got_bins, want_bins), "bins differ"
+    # scores
+    s64, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values,
+                            case.depth, n_trees=case.n_trees)
+    f = s_fused.cpu().numpy()
+    t = s_two.cpu().numpy()
+    assert np.array_equal(f.view(np.uint32), t.view(np.uint32)), "fused != two-stage"
+    if exact:
+        assert np.array_equal(f, s32), "exact-arithmetic leaves must give bit-exact scores"
+    else:
+        err = np.abs(f.astype(np.float64) - s64)
+        tol = tolerance(case.leaf_values, case.depth)
+        assert err.max(initial=0.0) <= tol, (err.max(), tol)
+    # leaf indices: fingerprint of every document, and a window
+    if check_fp and case.n_trees > 0:
+        fp = m.index_fingerprint(bins, n).cpu().numpy().view(np.uint64)
+        want_fp = oracle.fingerprint(case.x, case.feature_index, case.thresholds, case.depth,
+                                     case.n_trees)
+        assert np.array_equal(fp, want_fp), "leaf-index fingerprints differ"
+    if idx_window and case.n_trees > 0:
+        d0, nd, t0, nt = idx_window
+        got = m.leaf_indices(bins, n, d0, nd, t0, nt).cpu().numpy().view(np.uint16)
+        want = oracle.leaf_indices(case.x, case.feature_index, case.thresholds, case.depth,
+                                   d0, nd, t0, nt)
+        assert np.array_equal(got, want)
+    torch.cuda.synchronize()
+    m.close()
+    return f
+
+
+@pytest.mark.parametrize("seed", range(1, 21))
+def test_c1_twenty_seeds(seed):
+    case = synth.make_case("c1", seed=seed)
+    full_check(case, idx_window=(0, case.n_docs, 0, case.n_trees))
+
+
+@pytest.mark.parametrize("n_docs", SPEC_DOC_COUNTS)
+def test_spec_doc_counts(n_docs):
+    case = synth.tiny_case(seed=100 + n_docs, n_docs=n_docs, n_features=37, ld=40, n_trees=83,
+                           depth=6, pool=16)
+    full_check(case, idx_window=(0, n_docs, 0, 83))
+
+
+@pytest.mark.parametrize("depth", list(range(0, 11)))
+def test_every_depth(depth):
+    case = synth.tiny_case(seed=200 + depth, n_docs=300, n_features=19, ld=20, n_trees=45,
+                           depth=depth, pool=12)
+    full_check(case, idx_window=(0, 300, 0, 45))
+
+
+@pytest.mark.parametrize("depth", [3, 6, 10])
+def test_exact_arithmetic_leaves_bit_exact(depth):
+    case = synth.tiny_case(seed=300 + depth, n_docs=777, n_features=24, n_trees=210,
+                           depth=depth, pool=20, exact_leaves=True)
+    full_check(case, exact=True)
+
+
+def test_special_values_ties_nan_zero_denormal_inf():
+    case = synth.tiny_case(seed=41, n_docs=1000, n_features=16, n_trees=128, depth=6, pool=10)
+    x = case.x
+    rng = np.random.default_rng(3)
+    for _ in range(3000):  # exact ties: a factor equal to a threshold on it
+        k = rng.integers(case.feature_index.size)
+        x[rng.integers(case.n_docs), case.feature_index[k]] = case.thresholds[k]
+    specials = np.array([np.nan, -0.0, 0.0, 1e-45, -1e-45, 1e-40, np.inf, -np.inf,
+                         np.finfo(np.float32).max, -np.finfo(np.float32).max], np.float32)
+    for _ in range(3000):
+        x[rng.integers(case.n_docs), rng.integers(16)] = specials[rng.integers(specials.size)]
+    # thresholds that are themselves +-0.0 and denormal
+    case.thresholds[:20:4] = np.float32(-0.0)
+    case.thresholds[1:20:4] = np.float32(0.0)
+    case.thresholds[2:20:4] = np.float32(1e-45)
+    full_check(case, idx_window=(0, 1000, 0, 128))
+
+
+@pytest.mark.parametrize("n_borders", [127, 128, 200, 254])
+def test_many_borders_split_columns(n_borders):
+    # one factor carries n_borders distinct thresholds (> 127 uses two code columns)
+    rng = np.random.default_rng(n_borders)
+    F, T, d, D = 8, 96, 6, 700
+    pool = np.sort(rng.standard_normal(n_borders).astype(np.float32))
+    fi = rng.integers(0, F, T * d).astype(np.int32)
+    thr = rng.standard_normal(T * d).astype(np.float32)
+    first = np.arange(n_borders)
+    fi[first] = 3
+    thr[first] = pool
+    hot = rng.random(T * d) < 0.3
+    fi[hot] = 3
+    thr[hot] = pool[rng.integers(0, n_borders, hot.sum())]
+    x = rng.standard_normal((D, F)).astype(np.float32)
+    x[::3, 3] = pool[rng.integers(0, n_borders, x[::3, 3].size)]  # ties on the hot factor
+    lv = rng.normal(0, 0.01, T << d).astype(np.float32)
+    case = synth.ForestCase("split", x, F, fi, thr, lv, d, T)
+    full_check(case, idx_window=(0, D, 0, T))
+
+
+def test_zero_docs_zero_trees_depth0():
+    import torch
+    case = synth.tiny_case(seed=51, n_docs=10, n_features=8, n_trees=0, depth=6)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    assert np.all(m.score(x).cpu().numpy() == 0.0)
+    assert m.n_used == 0
+    empty = torch.empty((0, 8), dtype=torch.float32, device="cuda")
+    assert m.score(empty).numel() == 0
+    m.close()
+    case = synth.tiny_case(seed=52, n_docs=130, n_features=8, n_trees=5, depth=0)
+    full_check(case)
+
+
+def test_ld_padding_and_ragged_features():
+    case = synth.tiny_case(seed=61, n_docs=513, n_features=45, ld=64, n_trees=70, depth=5,
+                           pool=9)
+    case.x[:, 45:] = np.nan  # padding columns must never be read as factors
+    full_check(case, idx_window=(100, 300, 3, 60))
+
+
+def test_invalid_factor_layouts_rejected():
+    import torch
+    from paper_2205_07307_b200 import OdfError
+    case = synth.tiny_case(seed=62, n_docs=64, n_features=6, ld=6, n_trees=4, depth=3)
+    m = cuda_model(case)
+    x = torch.from_numpy(case.x).cuda()
+    with pytest.raises(OdfError) as e:
+        m.score(x)  # ld = 6 is not a multiple of 4 (TMA row alignment)
+    assert e.value.status == 1
+    m.close()
+
+
+def test_too_many_borders_unsupported():
+    from paper_2205_07307_b200 import Model, OdfError
+    thr = np.arange(255, dtype=np.float32)
+    fi = np.zeros(255, np.int32)
+    lv = np.zeros(255 * 2, np.float32)
+    with pytest.raises(OdfError) as e:
+        Model(fi, thr, lv, 1, 1)
+    assert e.value.status == 2
+
+
+def test_score_independent_of_batch_and_offset():
+    import torch
+    case = synth.make_case("c2", n_docs=5000, n_trees=300)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    full = m.score(x).cpu().numpy()
+    for a, b in [(0, 1), (1, 130), (127, 4000), (4999, 5000), (333, 4444)]:
+        part = m.score(x[a:b].contiguous()).cpu().numpy()
+        assert np.array_equal(part.view(np.uint32), full[a:b].view(np.uint32)), (a, b)
+    torch.cuda.synchronize()
+    m.close()
+
+
+def test_score_host_e2e_matches_device():
+    import torch
+    case = synth.make_case("c2", n_docs=20000, n_trees=200)
+    m = cuda_model(case)
+    dev = m.score(to_dev(case.x)).cpu().numpy()
+    xh = torch.from_numpy(case.x).pin_memory()
+    host = m.score_host(xh, chunk_docs=3000)
+    assert np.array_equal(host.numpy().view(np.uint32), dev.view(np.uint32))
+    host2 = m.score_host(case.x, chunk_docs=1 << 20)
+    assert np.array_equal(host2.view(np.uint32), dev.view(np.uint32))
+    m.close()
+
+
+def test_concurrent_streams_one_model():
+    import torch
+    case = synth.make_case("c2", n_docs=3000, n_trees=500)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    ref = m.score(x).cpu().numpy()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = []
+    for s in streams:
+        with torch.cuda.stream(s):
+            outs.append(m.score(x, stream=s))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    m.close()
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json sizes, in the launch configuration bench.py times
+# ---------------------------------------------------------------------------
+def _sampled_full_size(name, n_sample=1500, fp_docs=2048):
+    import torch
+    case = synth.make_case(name)
+    n = case.n_docs
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    bins, s_fused, s_two = run_cuda(m, x, n)
+    f = s_fused.cpu().numpy()
+    assert np.array_equal(f.view(np.uint32), s_two.cpu().numpy().view(np.uint32))
+    rng = np.random.default_rng(99)
+    rows = np.unique(np.concatenate([rng.integers(0, n, n_sample), [0, 1, 127, 128, n - 1]]))
+    s64 = oracle.score_rows(case.x, rows, case.feature_index, case.thresholds, case.leaf_values,
+                            case.depth)
+    err = np.abs(f[rows].astype(np.float64) - s64)
+    assert err.max() <= tolerance(case.leaf_values, case.depth), err.max()
+    # bins of the sampled rows, bit-exact
+    per, flat, counts, offs = oracle.borders(case.feature_index, case.thresholds, case.n_features)
+    used = np.flatnonzero(counts > 0)
+    want = oracle.bins(case.x[rows], case.n_features, flat, counts, offs)[:, used]
+    canon = m.canonical_bins(bins, n)
+    got = canon[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert np.array_equal(got, want)
+    # leaf-index fingerprints of a window of documents (every tree), bit-exact
+    d0 = n - fp_docs
+    fp = m.index_fingerprint(bins, n).cpu().numpy().view(np.uint64)
+    want_fp = oracle.fingerprint(case.x[d0:], case.feature_index, case.thresholds, case.depth,
+                                 case.n_trees)
+    assert np.array_equal(fp[d0:], want_fp)
+    # a leaf-index window
+    got_idx = m.leaf_indices(bins, n, 1000, 64, case.n_trees - 100, 100).cpu().numpy().view(np.uint16)
+    want_idx = oracle.leaf_indices(case.x, case.feature_index, case.thresholds, case.depth,
+                                   1000, 64, case.n_trees - 100, 100)
+    assert np.array_equal(got_idx, want_idx)
+    m.close()
+    del x, bins
+    torch.cuda.empty_cache()
+
+
+def test_c2_full_size():
+    _sampled_full_size("c2")
+
+
+def test_c3_full_size():
+    _sampled_full_size("c3", n_sample=600)
+
+
+def test_c4_full_size():
+    _sampled_full_size("c4", n_sample=600)
