@@ -57,13 +57,13 @@ odf_status cuda_fail(cudaError_t e, const char *what)
     return fail(ODF_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+uint32_t skew_h(uint32_t p) { return p + (p >> 5); }  // as skew() in odf_kernels.cu
 uint32_t align_up(uint64_t v, uint64_t a) { return static_cast<uint32_t>((v + a - 1) / a * a); }
 
 struct Plan {
-    uint32_t off_bins = 0, off_borders = 0, off_ring = 0, off_red = 0, off_bars = 0;
-    uint32_t slot_bytes = 0;
+    uint32_t off_bins = 0, off_ring = 0, off_red = 0, off_bars = 0;
+    uint32_t slot_bytes = 0, off_meta = 0, off_bord = 0;
     int stages = 0, fsub = 1;
-    bool bsm = false;
     size_t smem = 0;
     int grid_per_sm = 1;
 };
@@ -82,6 +82,7 @@ struct odf_model {
     int32_t max_borders = 0;
     int64_t total_borders = 0;
     int32_t n_fchunks = 0, border_floats = 0;
+    uint32_t bord_stride = 0;  // max bytes of one sub-tile's border arrays (16-aligned)
     int32_t tc = 16, n_tchunks = 0;
     uint32_t chunk_bytes = 0, desc_bytes = 0, table_stride = 0;
     int64_t dev_bytes = 0;
@@ -89,6 +90,7 @@ struct odf_model {
     float *d_borders = nullptr;
     uint8_t *d_chunks = nullptr;
     uint2 *d_splits = nullptr;
+    uint2 *d_bchunk = nullptr;
     Plan fused, binz, apply;
     // odf_score_host staging
     std::mutex host_mu;
@@ -108,52 +110,46 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
 {
     const uint32_t cols = (mode == MODE_BINARIZE) ? m.n_used : m.n_cols;
     const uint32_t bins = align_up(static_cast<uint64_t>(cols) * kTile, 1024);
-    const uint32_t red = (mode == MODE_BINARIZE) ? 0 : kRedBytes;
+    const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, kRedBytes);
     const uint32_t bars = 256;
-    const uint32_t borders = align_up(static_cast<uint64_t>(m.border_floats) * 4, 128);
+    // a factor sub-tile travels as [16 KB box][512 B fmeta][its border arrays]
+    const uint32_t unit = kFSubBytes + kMetaBytes + m.bord_stride;
     uint32_t slot;
     int smax;
     if (mode == MODE_BINARIZE) {
-        slot = kFSubBytes;
-        smax = 8;
+        slot = align_up(unit, 1024);
+        smax = 6;
     } else if (mode == MODE_APPLY) {
         slot = align_up(m.chunk_bytes, 1024);
         smax = 4;
     } else {
-        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), kFSubBytes);
+        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(unit, 1024));
         smax = 4;
     }
     const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
-    const int64_t fixed = static_cast<int64_t>(bins) + red + bars;
-    const bool want_borders = (mode != MODE_APPLY) && m.border_floats > 0;
-    int s_bsm = want_borders ? static_cast<int>((avail - fixed - borders) / slot) : -1;
-    int s_glb = static_cast<int>((avail - fixed) / slot);
-    pl.bsm = want_borders && s_bsm >= 3;
-    pl.stages = std::min(smax, pl.bsm ? s_bsm : s_glb);
+    const int64_t fixed = static_cast<int64_t>(bins_region) + bars;
+    pl.stages = std::min<int64_t>(smax, (avail - fixed) / slot);
     if (pl.stages < 2) {
         char b[256];
         snprintf(b, sizeof b,
-                 "shared memory: %u code columns x 128 B + %u B slots do not fit %d B "
-                 "(need >= 2 slots)",
-                 cols, slot, m.max_smem);
+                 "shared memory: %u code columns x 128 B + 2 x %u B slots do not fit %d B", cols,
+                 slot, m.max_smem);
         why = b;
         return false;
     }
     pl.slot_bytes = slot;
-    pl.fsub = static_cast<int>(slot / kFSubBytes);
-    if (pl.fsub < 1) pl.fsub = 1;
+    pl.fsub = std::max<int>(1, static_cast<int>(slot / unit));
+    pl.off_meta = pl.fsub * kFSubBytes;
+    pl.off_bord = pl.off_meta + pl.fsub * kMetaBytes;
     uint32_t off = 0;
     pl.off_ring = off;                    // ring first: TMA swizzle needs 1024 B alignment
     off += pl.stages * slot;
     pl.off_bins = off;
-    off += bins;
-    pl.off_borders = off;
-    if (pl.bsm) off += borders;
-    pl.off_red = off;
-    off += red;
+    pl.off_red = off;                     // reduction buffer aliases the bins (dead by then)
+    off += bins_region;
     pl.off_bars = off;
     off += bars;
-    pl.smem = off + 1024;
+    pl.smem = off;
     return true;
 }
 
@@ -188,7 +184,7 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.fmeta = m->d_fmeta;
     p.borders = m->d_borders;
     p.n_fchunks = m->n_used > 0 ? m->n_fchunks : 0;
-    p.border_floats = m->border_floats;
+    p.bchunk = m->d_bchunk;
     p.chunks = m->d_chunks;
     p.n_tchunks = m->n_tchunks;
     p.tc = m->tc;
@@ -201,14 +197,15 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.n_used = m->n_used;
     p.n_cols = m->n_cols;
     p.off_bins = pl.off_bins;
-    p.off_borders = pl.off_borders;
     p.off_ring = pl.off_ring;
     p.off_red = pl.off_red;
     p.off_bars = pl.off_bars;
     p.slot_bytes = pl.slot_bytes;
     p.stages = pl.stages;
     p.fsub_per_job = pl.fsub;
-    p.borders_smem = pl.bsm ? 1 : 0;
+    p.off_meta = pl.off_meta;
+    p.off_bord = pl.off_bord;
+    p.bord_stride = m->bord_stride;
     return p;
 }
 
@@ -251,6 +248,7 @@ void odf_free_model(odf_model *m)
     cudaFree(m->d_borders);
     cudaFree(m->d_chunks);
     cudaFree(m->d_splits);
+    cudaFree(m->d_bchunk);
     for (int i = 0; i < 2; ++i) {
         cudaFree(m->d_stage[i]);
         cudaFree(m->d_sstage[i]);
@@ -330,26 +328,70 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
     m->n_split = static_cast<int32_t>(splits.size());
     m->n_cols = m->n_used + m->n_split;
 
-    // ---- factor metadata + padded, skewed border arrays (binarize) ----
+    // ---- factor metadata + border arrays (binarize; kinds in odf_internal.h) ----
     m->n_fchunks = (n_features + kFSub - 1) / kFSub;
     std::vector<uint4> fmeta(static_cast<size_t>(m->n_fchunks) * kFSub, make_uint4(0, 0, 0, kNoCol));
     std::vector<float> bflat;
+    auto ceil_log2p1 = [](uint32_t mm) {
+        uint32_t L = 0;
+        while (((1u << L) - 1u) < mm) ++L;  // smallest L with 2^L - 1 >= m
+        return L;
+    };
+    // pairs (f, f+1), f even: LIN4 if both have <= 4 borders, else BIN padded to the pair's L
+    std::vector<uint32_t> kind(fmeta.size(), 0), Lof(fmeta.size(), 0);
+    for (size_t f = 0; f < fmeta.size(); f += 2) {
+        const uint32_t ma = f < static_cast<size_t>(n_features) ? static_cast<uint32_t>(borders[f].size()) : 0;
+        const uint32_t mb = f + 1 < static_cast<size_t>(n_features) ? static_cast<uint32_t>(borders[f + 1].size()) : 0;
+        if (ma == 0 && mb == 0) continue;
+        const uint32_t k = std::max(ma, mb) <= 4 ? 1u : 2u;
+        const uint32_t L = k == 2 ? ceil_log2p1(std::max(ma, mb)) : 0u;
+        kind[f] = kind[f + 1] = k;
+        Lof[f] = Lof[f + 1] = L;
+    }
     for (int32_t f : m->used_ids) {
         const auto &b = borders[f];
         const uint32_t mm = static_cast<uint32_t>(b.size());
-        uint32_t L = 0;
-        while (((1u << L) - 1u) < mm) ++L;  // 2^L - 1 >= m
-        const uint32_t n_pad = (1u << L) - 1u;
-        const uint32_t len = (n_pad - 1u) + ((n_pad - 1u) >> 5) + 1u;
         const uint32_t off = static_cast<uint32_t>(bflat.size());
-        bflat.resize(bflat.size() + len, INFINITY);
-        for (uint32_t pidx = 0; pidx < n_pad; ++pidx)
-            bflat[off + pidx + (pidx >> 5)] = pidx < mm ? b[pidx] : INFINITY;
-        fmeta[f] = make_uint4(off, L | (mm << 8), static_cast<uint32_t>(used_of[f]) * kTile,
+        if (kind[f] == 1) {
+            bflat.resize(off + 4, INFINITY);
+            for (uint32_t j = 0; j < mm; ++j) bflat[off + j] = b[j];
+        } else {
+            const uint32_t n_pad = (1u << Lof[f]) - 1u;
+            bflat.resize(off + skew_h(n_pad - 1u) + 1u, INFINITY);
+            for (uint32_t pidx = 0; pidx < n_pad; ++pidx)
+                bflat[off + skew_h(pidx)] = pidx < mm ? b[pidx] : INFINITY;
+        }
+        while (bflat.size() % 4) bflat.push_back(INFINITY);  // 16-byte aligned arrays
+        fmeta[f] = make_uint4(off, kind[f] | (Lof[f] << 8) | (mm << 16),
+                              static_cast<uint32_t>(used_of[f]) * kTile,
                               colB_of[f] >= 0 ? static_cast<uint32_t>(colB_of[f]) * kTile : kNoCol);
     }
-    while (bflat.size() % 4) bflat.push_back(INFINITY);
+    // the unused factor of a mixed pair searches its partner's array and stores nothing
+    for (size_t f = 0; f + 1 < fmeta.size(); f += 2) {
+        const bool ua = f < static_cast<size_t>(n_features) && !borders[f].empty();
+        const bool ub = f + 1 < static_cast<size_t>(n_features) && !borders[f + 1].empty();
+        if (ua && !ub) fmeta[f + 1] = make_uint4(fmeta[f].x, fmeta[f].y & 0xffffu, kNoCol, kNoCol);
+        if (ub && !ua) fmeta[f] = make_uint4(fmeta[f + 1].x, fmeta[f + 1].y & 0xffffu, kNoCol, kNoCol);
+    }
     m->border_floats = static_cast<int32_t>(bflat.size());
+    // per sub-tile border ranges; fmeta.x becomes relative to its sub-tile's range
+    std::vector<uint2> bchunk(m->n_fchunks, make_uint2(0, 0));
+    for (int32_t c = 0; c < m->n_fchunks; ++c) {
+        uint32_t lo = UINT32_MAX, hi = 0;
+        for (int32_t f = c * kFSub; f < (c + 1) * kFSub; ++f) {
+            if ((fmeta[f].y & 0xffu) == 0) continue;
+            const uint32_t kf = fmeta[f].y & 0xffu;
+            const uint32_t L = (fmeta[f].y >> 8) & 0xffu;
+            const uint32_t len = kf == 1 ? 4u : skew_h((1u << L) - 2u) + 1u;
+            lo = std::min(lo, fmeta[f].x);
+            hi = std::max(hi, (fmeta[f].x + len + 3u) & ~3u);
+        }
+        if (hi == 0) continue;
+        for (int32_t f = c * kFSub; f < (c + 1) * kFSub; ++f)
+            if ((fmeta[f].y & 0xffu) != 0) fmeta[f].x -= lo;
+        bchunk[c] = make_uint2(lo * 4u, (hi - lo) * 4u);
+        m->bord_stride = std::max(m->bord_stride, (hi - lo) * 4u);
+    }
 
     // ---- tree chunks: descriptors + reversed leaf tables ----
     const int dstride = ((depth + 1) & ~1) * 8;
@@ -407,7 +449,8 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
     if ((e = up(reinterpret_cast<void **>(&m->d_fmeta), fmeta.data(), fmeta.size() * sizeof(uint4))) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_borders), bflat.data(), bflat.size() * 4)) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_chunks), chunks.data(), chunks.size())) != cudaSuccess ||
-        (e = up(reinterpret_cast<void **>(&m->d_splits), splits.data(), splits.size() * sizeof(uint2))) != cudaSuccess) {
+        (e = up(reinterpret_cast<void **>(&m->d_splits), splits.data(), splits.size() * sizeof(uint2))) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_bchunk), bchunk.data(), bchunk.size() * sizeof(uint2))) != cudaSuccess) {
         odf_model *raw = m.release();
         odf_free_model(raw);
         return e == cudaErrorMemoryAllocation ? fail(ODF_E_NOMEM, "device allocation failed")
@@ -448,7 +491,7 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->model_device_bytes = m->dev_bytes;
     info->max_borders = m->max_borders;
     info->total_borders = m->total_borders;
-    info->borders_in_smem = m->fused.bsm ? 1 : 0;
+    info->borders_in_smem = 0;
     info->stages_fused = m->fused.stages;
     info->smem_fused = static_cast<int32_t>(m->fused.smem);
     info->num_sms = m->num_sms;

@@ -13,6 +13,7 @@ constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kThreads = kConsumerThreads + 32;  // + 1 producer (TMA) warp
 constexpr int kFSub = 32;                  // factors per TMA sub-tile (32 x 4 B = 128 B rows)
 constexpr uint32_t kFSubBytes = kTile * kFSub * 4;  // 16 KB TMA box [128 docs x 32 factors]
+constexpr uint32_t kMetaBytes = kFSub * 16;         // fmeta of one sub-tile
 constexpr uint32_t kRedBytes = kConsumerWarps * kTile * 4;
 constexpr uint32_t kNoCol = 0xFFFFFFFFu;
 
@@ -21,12 +22,15 @@ enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 // Per-launch parameters (passed by value; all pointers are device pointers).
 struct KParams {
     // ---- binarization (stage 1) ----
-    const uint4 *fmeta;     // [n_fchunks*32] per raw factor: {border_off (floats), L | m<<8,
-                            //  colA*128, colB*128 or kNoCol}; L == 0 -> unused factor
-    const float *borders;   // per used factor: sorted borders padded to 2^L-1 with +inf,
+    const uint4 *fmeta;     // [n_fchunks*32] per raw factor: {border_off (floats, 16 B aligned),
+                            //  kind | L<<8 | m<<16, colA*128, colB*128 or kNoCol}
+                            //  kind: 0 unused, 1 LIN4, 2 LIN8, 3 BIN, 4 PAIR(first), 5 PAIRED
+    const float *borders;   // per used factor: LIN4/LIN8 -> 4/8 sorted borders padded with
+                            // +inf; BIN/PAIR -> sorted borders padded to 2^L-1 with +inf,
                             // stored skewed (position p at p + (p >> 5))
+    const uint2 *bchunk;    // [n_fchunks] {byte offset into borders, bytes} of each sub-tile's
+                            // border arrays (fmeta.x is relative to that offset)
     int32_t n_fchunks;      // ceil(n_features / 32), 0 if no used factor
-    int32_t border_floats;  // floats in `borders`
     // ---- apply (stage 2) ----
     const uint8_t *chunks;  // [n_tchunks][chunk_bytes]: descriptors then reversed leaf tables
     int32_t n_tchunks;
@@ -42,11 +46,11 @@ struct KParams {
     uint8_t *bins_out;       // blocked bins (binarize)
     float *scores;
     // ---- shared-memory plan (byte offsets from the 1 KB aligned base) ----
-    uint32_t off_bins, off_borders, off_ring, off_red, off_bars;
+    uint32_t off_bins, off_ring, off_red, off_bars;
     uint32_t slot_bytes;
+    uint32_t off_meta, off_bord, bord_stride;  // within a factor job's slot
     int32_t stages;
-    int32_t fsub_per_job;    // TMA sub-tiles per factor job (slot_bytes / 16 KB)
-    int32_t borders_smem;    // 1: borders copied to shared memory at kernel start
+    int32_t fsub_per_job;    // factor sub-tiles per job (tiles, then metas, then borders)
     // ---- index export / fingerprint ----
     int64_t doc0, ndoc, tree0, ntree;
     uint16_t *idx_out;

@@ -30,68 +30,41 @@
 namespace odf {
 
 // ---------------------------------------------------------------------------
-// PTX helpers (shared-window 32-bit addresses throughout)
+// Shared memory: one dynamic buffer, addressed by byte OFFSETS from its start.
+// Plain C++ loads/stores (compiler-schedulable LDS/STS); the asynchronous
+// proxy (TMA, bulk copies, mbarriers) gets the absolute shared-window address.
+// The buffer is 1024-byte aligned in the shared window (checked at kernel
+// start), which the 128B TMA swizzle and the 256-byte leaf-table trick need.
 // ---------------------------------------------------------------------------
+extern __shared__ __align__(1024) uint8_t smem_raw[];
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p)
 {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+__device__ __forceinline__ uint32_t sabs(uint32_t off) { return smem_addr(smem_raw) + off; }
+template <class T>
+__device__ __forceinline__ T sld(uint32_t off)
 {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
+    return *reinterpret_cast<const T *>(smem_raw + off);
 }
-__device__ __forceinline__ float lds_f32(uint32_t a)
+template <class T>
+__device__ __forceinline__ void sst(uint32_t off, T v)
 {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-    return v;
+    *reinterpret_cast<T *>(smem_raw + off) = v;
 }
-__device__ __forceinline__ uint2 lds_v2u(uint32_t a)
-{
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint4 lds_v4u(uint32_t a)
-{
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ float4 lds_v4f(uint32_t a)
-{
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v)
-{
-    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
-{
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sts_f32(uint32_t a, float v)
-{
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) { return sld<uint32_t>(a); }
+__device__ __forceinline__ float lds_f32(uint32_t a) { return sld<float>(a); }
+__device__ __forceinline__ uint2 lds_v2u(uint32_t a) { return sld<uint2>(a); }
+__device__ __forceinline__ uint4 lds_v4u(uint32_t a) { return sld<uint4>(a); }
+__device__ __forceinline__ float4 lds_v4f(uint32_t a) { return sld<float4>(a); }
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { sst<uint8_t>(a, static_cast<uint8_t>(v)); }
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) { sst<uint32_t>(a, v); }
 __device__ __forceinline__ void sts_v4f(uint32_t a, float x, float y, float z, float w)
 {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z),
-                 "f"(w)
-                 : "memory");
+    sst<float4>(a, make_float4(x, y, z, w));
 }
-__device__ __forceinline__ void sts_v4u(uint32_t a, uint4 v)
-{
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w)
-                 : "memory");
-}
+__device__ __forceinline__ void sts_v4u(uint32_t a, uint4 v) { sst<uint4>(a, v); }
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
 {
     uint32_t d;
@@ -102,18 +75,20 @@ __device__ __forceinline__ void named_bar_consumers()
 {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerThreads) : "memory");
 }
+// mbarriers / bulk copies: arguments are buffer OFFSETS
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
 {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sabs(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
 {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sabs(bar)),
+                 "r"(bytes)
                  : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sabs(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
@@ -121,7 +96,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
         "{\n\t.reg .pred p;\n"
         "ODF_WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra ODF_WAIT_%=;\n}\n" ::"r"(bar),
+        "@!p bra ODF_WAIT_%=;\n}\n" ::"r"(sabs(bar)),
         "r"(parity)
         : "memory");
 }
@@ -138,22 +113,22 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
 {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(sabs(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(sabs(bar))
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
 {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
+            "r"(sabs(dst)),
+        "l"(src), "r"(bytes), "r"(sabs(bar))
         : "memory");
 }
 __device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src, uint32_t bytes)
 {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
-                 "r"(bytes)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(sabs(src)), "r"(bytes)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -170,68 +145,137 @@ __device__ __forceinline__ void bulk_wait_all()
 // Stage 1: binarization of one 128-doc x 32-factor sub-tile
 // ---------------------------------------------------------------------------
 // The TMA box lands with SWIZZLE_128B: 16-byte chunk q of row r sits at chunk
-// q ^ (r & 7), so the LDS.128 of a warp (32 rows, one chunk) is conflict-free.
-// Warp w handles documents (w&3)*32 + lane and factor quads (w>>2), (w>>2)+4.
-// bin(x) = #{j : !(x < b_j)} by a branchless search over the factor's sorted
-// borders padded to 2^L - 1 entries with +inf (the predicate !(x < b) is a
-// prefix of the sorted array for every x, NaN and +inf included; the result is
-// then clamped to m).  The 4 searches of a quad run interleaved.
-template <bool CODES, bool BSMEM>
-__device__ __forceinline__ void binarize_sub(uint32_t stage, int fchunk, const KParams &p,
-                                             uint32_t bins, uint32_t bsm, int warp, int lane)
+// q ^ (r & 7), so warp-wide reads of one chunk (32 rows) are conflict-free.
+// Warp w handles documents (w&3)*32 + lane and the factor quads (w>>2) and
+// (w>>2)+4 of the sub-tile, i.e. 4 pairs of adjacent factors (2 per LDS.64).
+//
+// bin(x) = #{j : !(x < b_j)}.  Each pair of adjacent factors is
+// evaluated with one straight-line code path chosen by the model compiler
+// (fmeta.y = kind | L<<8 | m<<16, identical kind/L for both factors of a pair):
+//   LIN4  both m <= 4: count !(x < b_j) over 4 borders padded with +inf
+//         (warp-uniform broadcast loads, no dependent chain);
+//   BIN   branchless search over the sorted borders padded to 2^L - 1 with
+//         +inf, both factors padded to the pair's L and searched interleaved
+//         (two independent chains per lane); arrays are stored skewed
+//         (position p at p + (p >> 5)) so the lanes of one step hit distinct banks.
+// For every x the predicate !(x < b) is a prefix of the padded sorted array
+// (NaN and +inf: the whole array), so every count is min(count, m).
+// An unused factor of a pair searches its partner's array and stores nothing.
+enum : uint32_t { BK_SKIP = 0, BK_LIN4 = 1, BK_BIN = 2 };
+
+__host__ __device__ constexpr uint32_t skew(uint32_t p) { return p + (p >> 5); }
+
+// all-ones if !(x < b) (unordered or >=: NaN counts), else 0
+__device__ __forceinline__ uint32_t not_less_mask(float x, float b)
 {
-    const int doc = ((warp & 3) << 5) | lane;
-    const uint32_t row = stage + doc * 128;
+    uint32_t r;
+    asm("set.geu.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(x), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t ge4(float x, float4 b)
+{
+    return 0u - not_less_mask(x, b.x) - not_less_mask(x, b.y) - not_less_mask(x, b.z) -
+           not_less_mask(x, b.w);
+}
+
+// One step of the branchless search for 4 independent chains (2 factors x 2 docs).
+template <int L>
+__device__ __forceinline__ void search4(const float x[4], uint32_t pos[4])
+{
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int q = (warp >> 2) + 4 * h;
-        const int f0 = fchunk * kFSub + q * 4;
-        uint4 m[4];
+    for (int st = L - 1; st >= 0; --st) {
+        const uint32_t s = 1u << st;
+        float b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) m[j] = __ldg(p.fmeta + f0 + j);
-        int L[4];
-        int lmax = 0;
+        for (int c = 0; c < 4; ++c) b[c] = lds_f32(pos[c] + 4u * skew(s - 1));
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            L[j] = static_cast<int>(m[j].y & 0xffu);
-            lmax = max(lmax, L[j]);
-        }
-        if (lmax == 0) continue;  // warp-uniform: no used factor in this quad
-        const float4 v = lds_v4f(row + ((q ^ (doc & 7)) << 4));
-        const float x[4] = {v.x, v.y, v.z, v.w};
-        uint32_t pos[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) pos[j] = m[j].x * 4u;
-        for (int st = lmax - 1; st >= 0; --st) {
-            const uint32_t s = 1u << st;
-            const uint32_t off = 4u * ((s - 1) + ((s - 1) >> 5));  // skewed position of s-1
-            const uint32_t inc = 4u * (s + (s >> 5));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (L[j] > st) {
-                    float b;
-                    if (BSMEM)
-                        b = lds_f32(bsm + pos[j] + off);
-                    else
-                        b = __ldg(reinterpret_cast<const float *>(
-                            reinterpret_cast<const char *>(p.borders) + pos[j] + off));
-                    if (!(x[j] < b)) pos[j] += inc;  // condition false -> border counted
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (L[j] == 0) continue;
-            const uint32_t ip = (pos[j] - m[j].x * 4u) >> 2;  // skewed index
-            const uint32_t idx = ip - ip / 33u;                // unskew (idx < 1056)
-            const uint32_t bin = min(idx, m[j].y >> 8);
-            if (CODES) {
-                sts_u8(bins + m[j].z + doc, min(bin, 127u));
-                if (m[j].w != kNoCol) sts_u8(bins + m[j].w + doc, bin > 127u ? bin - 127u : 0u);
-            } else {
-                sts_u8(bins + m[j].z + doc, bin);
-            }
-        }
+        for (int c = 0; c < 4; ++c) pos[c] += !(x[c] < b[c]) ? 4u * (s + (s >> 5)) : 0u;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t pos0, uint32_t m)
+{
+    uint32_t idx = (pos - pos0) >> 2;
+    if (L > 5) idx -= idx / 33u;  // unskew (idx < 264)
+    return min(idx, m);
+}
+
+template <bool CODES>
+__device__ __forceinline__ void store_bin(uint32_t bins, const uint4 &m, int doc, uint32_t bin)
+{
+    if (m.z == kNoCol) return;  // unused factor of a pair
+    if (CODES) {
+        sts_u8(bins + m.z + doc, min(bin, 127u));
+        if (m.w != kNoCol) sts_u8(bins + m.w + doc, max(bin, 127u) - 127u);
+    } else {
+        sts_u8(bins + m.z + doc, bin);
+    }
+}
+
+// x = {a@doc0, a@doc1, b@doc0, b@doc1}
+template <bool CODES, int L>
+__device__ __forceinline__ void bin_pair(const float x[4], const uint4 &ma, const uint4 &mb,
+                                         uint32_t bord, uint32_t bins, int d0, int d1)
+{
+    const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
+    uint32_t pos[4] = {a0, a0, b0, b0};
+    search4<L>(x, pos);
+    store_bin<CODES>(bins, ma, d0, pos_to_bin<L>(pos[0], a0, ma.y >> 16));
+    store_bin<CODES>(bins, ma, d1, pos_to_bin<L>(pos[1], a0, ma.y >> 16));
+    store_bin<CODES>(bins, mb, d0, pos_to_bin<L>(pos[2], b0, mb.y >> 16));
+    store_bin<CODES>(bins, mb, d1, pos_to_bin<L>(pos[3], b0, mb.y >> 16));
+}
+
+template <bool CODES>
+__device__ __forceinline__ void pair_dispatch(const float x[4], const uint4 &ma, const uint4 &mb,
+                                              uint32_t bord, uint32_t bins, int d0, int d1)
+{
+    const uint32_t kind = ma.y & 0xffu;
+    if (kind == BK_SKIP) return;  // warp-uniform
+    if (kind == BK_LIN4) {
+        const float4 ba = lds_v4f(bord + ma.x * 4u);
+        const float4 bb = lds_v4f(bord + mb.x * 4u);
+        store_bin<CODES>(bins, ma, d0, min(ge4(x[0], ba), ma.y >> 16));
+        store_bin<CODES>(bins, ma, d1, min(ge4(x[1], ba), ma.y >> 16));
+        store_bin<CODES>(bins, mb, d0, min(ge4(x[2], bb), mb.y >> 16));
+        store_bin<CODES>(bins, mb, d1, min(ge4(x[3], bb), mb.y >> 16));
+        return;
+    }
+    switch ((ma.y >> 8) & 0xffu) {
+    case 1: bin_pair<CODES, 1>(x, ma, mb, bord, bins, d0, d1); break;
+    case 2: bin_pair<CODES, 2>(x, ma, mb, bord, bins, d0, d1); break;
+    case 3: bin_pair<CODES, 3>(x, ma, mb, bord, bins, d0, d1); break;
+    case 4: bin_pair<CODES, 4>(x, ma, mb, bord, bins, d0, d1); break;
+    case 5: bin_pair<CODES, 5>(x, ma, mb, bord, bins, d0, d1); break;
+    case 6: bin_pair<CODES, 6>(x, ma, mb, bord, bins, d0, d1); break;
+    case 7: bin_pair<CODES, 7>(x, ma, mb, bord, bins, d0, d1); break;
+    default: bin_pair<CODES, 8>(x, ma, mb, bord, bins, d0, d1); break;
+    }
+}
+
+// tile: the 16 KB factor box; meta: its 32 fmeta entries (512 B); bord: its
+// factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot.
+// Warp w: factor quad q = w >> 1 (two pairs) for documents 64*(w&1) + lane and
+// + 32: 4 independent search chains per lane per pair.
+template <bool CODES>
+__device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
+                                             uint32_t bins, int warp, int lane)
+{
+    const int q = warp >> 1;
+    const int d0 = ((warp & 1) << 6) | lane, d1 = d0 + 32;
+    const uint4 m0 = lds_v4u(meta + 64u * q), m1 = lds_v4u(meta + 64u * q + 16u);
+    const uint4 m2 = lds_v4u(meta + 64u * q + 32u), m3 = lds_v4u(meta + 64u * q + 48u);
+    if (((m0.y | m2.y) & 0xffu) == BK_SKIP) return;  // warp-uniform: no used factor in the quad
+    const float4 v0 = lds_v4f(tile + d0 * 128 + ((q ^ (d0 & 7)) << 4));
+    const float4 v1 = lds_v4f(tile + d1 * 128 + ((q ^ (d1 & 7)) << 4));
+    {
+        const float x[4] = {v0.x, v1.x, v0.y, v1.y};
+        pair_dispatch<CODES>(x, m0, m1, bord, bins, d0, d1);
+    }
+    {
+        const float x[4] = {v0.z, v1.z, v0.w, v1.w};
+        pair_dispatch<CODES>(x, m2, m3, bord, bins, d0, d1);
     }
 }
 
@@ -353,19 +397,18 @@ __device__ __forceinline__ void expand_splits(const KParams &p, uint32_t bins, i
 // ---------------------------------------------------------------------------
 // Main persistent kernel: MODE_FUSED (K3), MODE_BINARIZE (K1), MODE_APPLY (K2)
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH, bool BSMEM>
+template <int MODE, int DEPTH>
 __global__ void __launch_bounds__(kThreads, 1)
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
-    extern __shared__ uint8_t smem_raw[];
     constexpr bool HAS_A = MODE != MODE_APPLY;
     constexpr bool HAS_B = MODE != MODE_BINARIZE;
-    const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    if (smem_addr(smem_raw) & 1023u) __trap();  // alignment the TMA swizzle relies on
+    const uint32_t base = 0;
     const uint32_t bins = base + p.off_bins;
     const uint32_t ring = base + p.off_ring;
     const uint32_t red = base + p.off_red;
     const uint32_t bars = base + p.off_bars;
-    const uint32_t bsm = base + p.off_borders;
     const int S = p.stages;
     const uint32_t bins_full = bars + 16u * S, bins_empty = bins_full + 8u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -381,10 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(bins_full, 1);
         mbar_init(bins_empty, kConsumerWarps);
         fence_barrier_init();
-    }
-    if (BSMEM) {
-        for (int i = threadIdx.x; i < p.border_floats; i += kThreads)
-            sts_f32(bsm + 4u * i, __ldg(p.borders + i));
     }
     __syncthreads();
 
@@ -407,10 +446,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(empty, ph ^ 1u);
                     const int c0 = j * p.fsub_per_job;
                     const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
-                    mbar_expect_tx(full, nsub * kFSubBytes);
-                    for (int s = 0; s < nsub; ++s)
-                        tma_load_2d(ring + slot * p.slot_bytes + s * kFSubBytes, &tmap,
-                                    (c0 + s) * kFSub, static_cast<int>(tile * kTile), full);
+                    const uint32_t sb = ring + slot * p.slot_bytes;
+                    uint32_t tx = 0;
+                    for (int s = 0; s < nsub; ++s) tx += kFSubBytes + kMetaBytes + p.bchunk[c0 + s].y;
+                    mbar_expect_tx(full, tx);
+                    for (int s = 0; s < nsub; ++s) {
+                        const int c = c0 + s;
+                        tma_load_2d(sb + s * kFSubBytes, &tmap, c * kFSub,
+                                    static_cast<int>(tile * kTile), full);
+                        bulk_g2s(sb + p.off_meta + s * kMetaBytes, p.fmeta + c * kFSub, kMetaBytes,
+                                 full);
+                        const uint2 bc = p.bchunk[c];
+                        if (bc.y)
+                            bulk_g2s(sb + p.off_bord + s * p.bord_stride,
+                                     reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, full);
+                    }
                     if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
                 }
                 for (int c = 0; c < n_bjobs; ++c) {
@@ -441,9 +491,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(full, ph);
                 const int c0 = j * p.fsub_per_job;
                 const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
+                const uint32_t sb = ring + slot * p.slot_bytes;
                 for (int s = 0; s < nsub; ++s)
-                    binarize_sub<MODE == MODE_FUSED, BSMEM>(ring + slot * p.slot_bytes + s * kFSubBytes,
-                                                            c0 + s, p, bins, bsm, warp, lane);
+                    binarize_sub<MODE == MODE_FUSED>(sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
+                                                     sb + p.off_bord + s * p.bord_stride, bins, warp,
+                                                     lane);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty);
                 if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -475,11 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(empty);
             if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
         }
-        if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
-            fence_proxy_async();  // expand_splits wrote bins; the next TMA overwrites them
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bins_empty);
-        }
+        // reduction buffer aliases the bins: wait until every warp is done with them
+        named_bar_consumers();
         sts_v4f(red + warp * (kTile * 4) + lane * 16, acc[0], acc[1], acc[2], acc[3]);
         named_bar_consumers();
         if (tid < kTile) {
@@ -489,7 +538,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t doc = tile * kTile + tid;
             if (doc < p.n_docs) p.scores[doc] = s;
         }
+        if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
+            fence_proxy_async();  // generic writes to the bins region precede the next TMA
+        }
         named_bar_consumers();
+        if (MODE == MODE_APPLY && tile_bins_bytes > 0 && lane == 0) mbar_arrive(bins_empty);
     }
     if (MODE == MODE_BINARIZE && tid == 0) bulk_wait_all();
 }
@@ -502,8 +555,8 @@ template <int DEPTH>
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_index_kernel(const KParams p, int fingerprint)
 {
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    if (smem_addr(smem_raw) & 1023u) __trap();
+    const uint32_t base = 0;
     const uint32_t bins = base;
     const uint32_t descs = base + ((static_cast<uint32_t>(p.n_cols) * kTile + 1023u) & ~1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -571,28 +624,26 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH, bool BSMEM>
+template <int MODE, int DEPTH>
 static const void *main_fn()
 {
-    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH, BSMEM>);
+    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH>);
 }
 
-#define ODF_DEPTH_TABLE(M, B)                                                              \
-    {main_fn<M, 0, B>(), main_fn<M, 1, B>(), main_fn<M, 2, B>(), main_fn<M, 3, B>(),       \
-     main_fn<M, 4, B>(), main_fn<M, 5, B>(), main_fn<M, 6, B>(), main_fn<M, 7, B>(),       \
-     main_fn<M, 8, B>(), main_fn<M, 9, B>(), main_fn<M, 10, B>()}
+#define ODF_DEPTH_TABLE(M)                                                                 \
+    {main_fn<M, 0>(), main_fn<M, 1>(), main_fn<M, 2>(), main_fn<M, 3>(), main_fn<M, 4>(),   \
+     main_fn<M, 5>(), main_fn<M, 6>(), main_fn<M, 7>(), main_fn<M, 8>(), main_fn<M, 9>(),   \
+     main_fn<M, 10>()}
 
-static const void *main_kernel(int mode, int depth, bool bsmem)
+static const void *main_kernel(int mode, int depth)
 {
-    static const void *fused[2][11] = {ODF_DEPTH_TABLE(MODE_FUSED, false),
-                                       ODF_DEPTH_TABLE(MODE_FUSED, true)};
-    static const void *apply[11] = ODF_DEPTH_TABLE(MODE_APPLY, false);
-    static const void *binz[2] = {main_fn<MODE_BINARIZE, 0, false>(),
-                                  main_fn<MODE_BINARIZE, 0, true>()};
+    static const void *fused[11] = ODF_DEPTH_TABLE(MODE_FUSED);
+    static const void *apply[11] = ODF_DEPTH_TABLE(MODE_APPLY);
+    static const void *binz = main_fn<MODE_BINARIZE, 0>();
     if (depth < 0 || depth > 10) return nullptr;
-    if (mode == MODE_FUSED) return fused[bsmem ? 1 : 0][depth];
+    if (mode == MODE_FUSED) return fused[depth];
     if (mode == MODE_APPLY) return apply[depth];
-    return binz[bsmem ? 1 : 0];
+    return binz;
 }
 
 template <int DEPTH>
@@ -611,25 +662,21 @@ static const void *index_kernel(int depth)
 cudaError_t prepare_kernels(int max_smem)
 {
     for (int d = 0; d <= 10; ++d) {
-        const void *fs[] = {main_kernel(MODE_FUSED, d, false), main_kernel(MODE_FUSED, d, true),
-                            main_kernel(MODE_APPLY, d, false), index_kernel(d)};
+        const void *fs[] = {main_kernel(MODE_FUSED, d), main_kernel(MODE_APPLY, d),
+                            index_kernel(d)};
         for (const void *f : fs) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
             if (e != cudaSuccess) return e;
         }
     }
-    for (int b = 0; b < 2; ++b) {
-        cudaError_t e = cudaFuncSetAttribute(main_kernel(MODE_BINARIZE, 0, b != 0),
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    return cudaFuncSetAttribute(main_kernel(MODE_BINARIZE, 0),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
 }
 
 int occupancy_main(int mode, int depth, size_t smem)
 {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, main_kernel(mode, depth, false), kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, main_kernel(mode, depth), kThreads,
                                                       smem) != cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
@@ -638,7 +685,7 @@ int occupancy_main(int mode, int depth, size_t smem)
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s)
 {
-    const void *f = main_kernel(mode, depth, p.borders_smem != 0);
+    const void *f = main_kernel(mode, depth);
     if (!f) return cudaErrorInvalidValue;
     KParams pc = p;
     CUtensorMap tm;
