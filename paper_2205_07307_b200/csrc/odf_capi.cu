@@ -111,7 +111,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
     const uint32_t cols = (mode == MODE_BINARIZE) ? m.n_used : m.n_cols;
     const uint32_t bins = align_up(static_cast<uint64_t>(cols) * kTile, 1024);
     const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, kRedBytes);
-    const uint32_t bars = 256;
+    const uint32_t bars = align_up(16u * 8 + 16 + 8u * m.n_fchunks, 128);  // + bchunk copy
     // a factor sub-tile travels as [16 KB box][512 B fmeta][its border arrays]
     const uint32_t unit = kFSubBytes + kMetaBytes + m.bord_stride;
     uint32_t slot;
@@ -124,7 +124,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
         smax = 4;
     } else {
         slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(unit, 1024));
-        smax = 4;
+        smax = 8;
     }
     const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
     const int64_t fixed = static_cast<int64_t>(bins_region) + bars;

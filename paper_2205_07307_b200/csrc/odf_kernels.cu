@@ -172,10 +172,21 @@ __device__ __forceinline__ uint32_t not_less_mask(float x, float b)
     asm("set.geu.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(x), "f"(b));
     return r;
 }
+// v += inc if !(x < b) (unordered or >=): one FSETP + one predicated IADD
+__device__ __forceinline__ void add_if_not_less(uint32_t &v, float x, float b, uint32_t inc)
+{
+    asm("{\n\t.reg .pred p;\n\tsetp.geu.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
+        : "+r"(v)
+        : "f"(x), "f"(b), "r"(inc));
+}
 __device__ __forceinline__ uint32_t ge4(float x, float4 b)
 {
-    return 0u - not_less_mask(x, b.x) - not_less_mask(x, b.y) - not_less_mask(x, b.z) -
-           not_less_mask(x, b.w);
+    uint32_t c = 0;
+    add_if_not_less(c, x, b.x, 1u);
+    add_if_not_less(c, x, b.y, 1u);
+    add_if_not_less(c, x, b.z, 1u);
+    add_if_not_less(c, x, b.w, 1u);
+    return c;
 }
 
 // One step of the branchless search for 4 independent chains (2 factors x 2 docs).
@@ -189,7 +200,7 @@ __device__ __forceinline__ void search4(const float x[4], uint32_t pos[4])
 #pragma unroll
         for (int c = 0; c < 4; ++c) b[c] = lds_f32(pos[c] + 4u * skew(s - 1));
 #pragma unroll
-        for (int c = 0; c < 4; ++c) pos[c] += !(x[c] < b[c]) ? 4u * (s + (s >> 5)) : 0u;
+        for (int c = 0; c < 4; ++c) add_if_not_less(pos[c], x[c], b[c], 4u * (s + (s >> 5)));
     }
 }
 
@@ -411,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t bars = base + p.off_bars;
     const int S = p.stages;
     const uint32_t bins_full = bars + 16u * S, bins_empty = bins_full + 8u;
+    const uint32_t bct = bins_empty + 8u;  // [n_fchunks] uint2 copy of p.bchunk
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_fjobs = HAS_A ? (p.n_fchunks + p.fsub_per_job - 1) / p.fsub_per_job : 0;
     const int n_bjobs = HAS_B ? p.n_tchunks : 0;
@@ -425,6 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(bins_empty, kConsumerWarps);
         fence_barrier_init();
     }
+    if (HAS_A)
+        for (int c = threadIdx.x; c < p.n_fchunks; c += kThreads) sst<uint2>(bct + 8u * c, p.bchunk[c]);
     __syncthreads();
 
     if (warp == kConsumerWarps) {
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
                     const uint32_t sb = ring + slot * p.slot_bytes;
                     uint32_t tx = 0;
-                    for (int s = 0; s < nsub; ++s) tx += kFSubBytes + kMetaBytes + p.bchunk[c0 + s].y;
+                    for (int s = 0; s < nsub; ++s) tx += kFSubBytes + kMetaBytes + sld<uint2>(bct + 8u * (c0 + s)).y;
                     mbar_expect_tx(full, tx);
                     for (int s = 0; s < nsub; ++s) {
                         const int c = c0 + s;
@@ -456,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     static_cast<int>(tile * kTile), full);
                         bulk_g2s(sb + p.off_meta + s * kMetaBytes, p.fmeta + c * kFSub, kMetaBytes,
                                  full);
-                        const uint2 bc = p.bchunk[c];
+                        const uint2 bc = sld<uint2>(bct + 8u * c);
                         if (bc.y)
                             bulk_g2s(sb + p.off_bord + s * p.bord_stride,
                                      reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, full);
