@@ -144,6 +144,21 @@ ODF_API odf_status odf_leaf_indices(const odf_model *m, const uint8_t *d_bins, i
 ODF_API odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
                                  uint64_t *d_fp, void *stream);
 
+/* Small-batch latency path (K4, config c5): the same scores as odf_score within
+ * the tolerance (the tree sum is split into `splits` contiguous chunk ranges per
+ * 128-document tile and combined in ascending split order: deterministic, but a
+ * different association than odf_score).  Two kernel
+ * launches: binarization spread over one CTA per (tile, 32-factor sub-tile), then
+ * the apply spread over `splits` CTAs per tile.  splits <= 0 picks a default
+ * (about 2 CTAs per SM).  d_workspace: device memory of at least
+ * odf_latency_workspace_bytes(m, n_docs, splits) bytes (same `splits`), owned by
+ * the caller; concurrent calls need distinct workspaces.  Same argument rules as
+ * odf_score.  Capturable in a CUDA graph.                                      */
+ODF_API size_t odf_latency_workspace_bytes(const odf_model *m, int64_t n_docs, int32_t splits);
+ODF_API odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t n_docs,
+                                     int64_t ld, float *d_scores, int32_t splits,
+                                     void *d_workspace, size_t workspace_bytes, void *stream);
+
 /* End-to-end from HOST memory: h_factors [n_docs x ld] fp32 (pinned or not;
  * pinned is faster) -> h_scores [n_docs].  Copies host->device, runs the fused
  * kernel, copies back, in chunks pipelined over two model-owned device staging

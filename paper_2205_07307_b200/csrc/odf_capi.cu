@@ -630,6 +630,79 @@ odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bins, int6
                      static_cast<cudaStream_t>(stream));
 }
 
+static int lat_splits(const odf_model *m, int64_t n_docs, int32_t splits)
+{
+    const int64_t tiles = std::max<int64_t>(1, (n_docs + kTile - 1) / kTile);
+    int64_t sp = splits > 0 ? splits : (2 * static_cast<int64_t>(m->num_sms)) / tiles;
+    sp = std::max<int64_t>(1, std::min<int64_t>(sp, std::max(1, m->n_tchunks)));
+    return static_cast<int>(std::min<int64_t>(sp, 1024));
+}
+
+static void lat_layout(const odf_model *m, int64_t n_docs, int sp, size_t off[4])
+{
+    const int64_t tiles = (n_docs + kTile - 1) / kTile;
+    auto a256 = [](size_t v) { return (v + 255) / 256 * 256; };
+    off[0] = 0;
+    off[1] = a256(static_cast<size_t>(tiles) * m->n_cols * kTile);
+    off[2] = off[1] + a256(static_cast<size_t>(tiles) * sp * kTile * 4);
+    off[3] = off[2] + a256(static_cast<size_t>(tiles) * 4);
+}
+
+size_t odf_latency_workspace_bytes(const odf_model *m, int64_t n_docs, int32_t splits)
+{
+    if (!m || n_docs < 0) return 0;
+    size_t off[4];
+    lat_layout(m, n_docs, lat_splits(m, n_docs, splits), off);
+    return off[3];
+}
+
+odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                             float *d_scores, int32_t splits, void *d_workspace,
+                             size_t workspace_bytes, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    odf_status st = check_factors(m, d_factors, n_docs, ld);
+    if (st != ODF_OK) return st;
+    if (n_docs == 0) return ok();
+    if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    const int sp = lat_splits(m, n_docs, splits);
+    size_t off[4];
+    lat_layout(m, n_docs, sp, off);
+    if (!d_workspace || workspace_bytes < off[3])
+        return fail(ODF_E_INVALID_ARG, "workspace of %zu bytes < odf_latency_workspace_bytes = %zu",
+                    workspace_bytes, off[3]);
+    if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0)
+        return fail(ODF_E_INVALID_ARG, "workspace not 256-byte aligned");
+    KParams p = base_params(m, m->fused);
+    p.n_docs = n_docs;
+    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.scores = d_scores;
+    uint8_t *ws = static_cast<uint8_t *>(d_workspace);
+    p.lat_codes = ws + off[0];
+    p.lat_partial = reinterpret_cast<float *>(ws + off[1]);
+    p.lat_counter = reinterpret_cast<uint32_t *>(ws + off[2]);
+    CUtensorMap tm;
+    const CUtensorMap *tmp = nullptr;
+    if (p.n_fchunks > 0) {
+        st = encode_tmap(m, d_factors, n_docs, ld, &tm);
+        if (st != ODF_OK) return st;
+        tmp = &tm;
+    }
+    const size_t smem_bin = kFSubBytes + kMetaBytes + align_up(m->bord_stride, 16) + 64;
+    const size_t smem_apply = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
+                              align_up(m->chunk_bytes, 1024) + kRedBytes;
+    if (smem_apply > static_cast<size_t>(m->max_smem))
+        return fail(ODF_E_UNSUPPORTED, "latency path: %zu B of shared memory > %d", smem_apply, m->max_smem);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != m->device) cudaSetDevice(m->device);
+    cudaError_t e = launch_latency(m->depth, p, tmp, sp, smem_bin, smem_apply,
+                                   static_cast<cudaStream_t>(stream));
+    if (prev != m->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "latency kernels");
+    return ok();
+}
+
 odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,
                           float *h_scores, int64_t chunk_docs, void *stream)
 {

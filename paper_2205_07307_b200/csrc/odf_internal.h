@@ -51,6 +51,10 @@ struct KParams {
     uint32_t off_meta, off_bord, bord_stride;  // within a factor job's slot
     int32_t stages;
     int32_t fsub_per_job;    // factor sub-tiles per job (tiles, then metas, then borders)
+    // ---- latency path (K4) workspace ----
+    uint8_t *lat_codes;      // [n_tiles][n_cols][128] 7-bit codes
+    float *lat_partial;      // [n_tiles][splits][128]
+    uint32_t *lat_counter;   // [n_tiles] tickets
     // ---- index export / fingerprint ----
     int64_t doc0, ndoc, tree0, ntree;
     uint16_t *idx_out;
@@ -61,6 +65,8 @@ cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap
                         size_t smem, cudaStream_t s);
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
                          cudaStream_t s);
+cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,
+                           size_t smem_bin, size_t smem_apply, cudaStream_t s);
 // Opt every kernel in to `smem` bytes of dynamic shared memory.
 cudaError_t prepare_kernels(int max_smem);
 // Number of co-resident CTAs per SM of a main kernel at `smem` bytes.

@@ -212,56 +212,70 @@ __device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t pos0, uint
     return min(idx, m);
 }
 
-template <bool CODES>
-__device__ __forceinline__ void store_bin(uint32_t bins, const uint4 &m, int doc, uint32_t bin)
+// Where the bins / codes of a tile go: shared memory (fused, binarize) or a
+// global [n_cols][128] block (latency path).
+struct SmemSink {
+    uint32_t base;
+    __device__ __forceinline__ void st(uint32_t off, uint32_t v) const { sts_u8(base + off, v); }
+};
+struct GmemSink {
+    uint8_t *base;
+    __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
+    {
+        base[off] = static_cast<uint8_t>(v);
+    }
+};
+
+template <bool CODES, class Sink>
+__device__ __forceinline__ void store_bin(const Sink &bins, const uint4 &m, int doc, uint32_t bin)
 {
     if (m.z == kNoCol) return;  // unused factor of a pair
     if (CODES) {
-        sts_u8(bins + m.z + doc, min(bin, 127u));
-        if (m.w != kNoCol) sts_u8(bins + m.w + doc, max(bin, 127u) - 127u);
+        bins.st(m.z + doc, min(bin, 127u));
+        if (m.w != kNoCol) bins.st(m.w + doc, max(bin, 127u) - 127u);
     } else {
-        sts_u8(bins + m.z + doc, bin);
+        bins.st(m.z + doc, bin);
     }
 }
 
 // x = {a@doc0, a@doc1, b@doc0, b@doc1}
-template <bool CODES, int L>
+template <bool CODES, int L, class Sink>
 __device__ __forceinline__ void bin_pair(const float x[4], const uint4 &ma, const uint4 &mb,
-                                         uint32_t bord, uint32_t bins, int d0, int d1)
+                                         uint32_t bord, const Sink &bins, int d0, int d1)
 {
     const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
     uint32_t pos[4] = {a0, a0, b0, b0};
     search4<L>(x, pos);
-    store_bin<CODES>(bins, ma, d0, pos_to_bin<L>(pos[0], a0, ma.y >> 16));
-    store_bin<CODES>(bins, ma, d1, pos_to_bin<L>(pos[1], a0, ma.y >> 16));
-    store_bin<CODES>(bins, mb, d0, pos_to_bin<L>(pos[2], b0, mb.y >> 16));
-    store_bin<CODES>(bins, mb, d1, pos_to_bin<L>(pos[3], b0, mb.y >> 16));
+    store_bin<CODES, Sink>(bins, ma, d0, pos_to_bin<L>(pos[0], a0, ma.y >> 16));
+    store_bin<CODES, Sink>(bins, ma, d1, pos_to_bin<L>(pos[1], a0, ma.y >> 16));
+    store_bin<CODES, Sink>(bins, mb, d0, pos_to_bin<L>(pos[2], b0, mb.y >> 16));
+    store_bin<CODES, Sink>(bins, mb, d1, pos_to_bin<L>(pos[3], b0, mb.y >> 16));
 }
 
-template <bool CODES>
+template <bool CODES, class Sink>
 __device__ __forceinline__ void pair_dispatch(const float x[4], const uint4 &ma, const uint4 &mb,
-                                              uint32_t bord, uint32_t bins, int d0, int d1)
+                                              uint32_t bord, const Sink &bins, int d0, int d1)
 {
     const uint32_t kind = ma.y & 0xffu;
     if (kind == BK_SKIP) return;  // warp-uniform
     if (kind == BK_LIN4) {
         const float4 ba = lds_v4f(bord + ma.x * 4u);
         const float4 bb = lds_v4f(bord + mb.x * 4u);
-        store_bin<CODES>(bins, ma, d0, min(ge4(x[0], ba), ma.y >> 16));
-        store_bin<CODES>(bins, ma, d1, min(ge4(x[1], ba), ma.y >> 16));
-        store_bin<CODES>(bins, mb, d0, min(ge4(x[2], bb), mb.y >> 16));
-        store_bin<CODES>(bins, mb, d1, min(ge4(x[3], bb), mb.y >> 16));
+        store_bin<CODES, Sink>(bins, ma, d0, min(ge4(x[0], ba), ma.y >> 16));
+        store_bin<CODES, Sink>(bins, ma, d1, min(ge4(x[1], ba), ma.y >> 16));
+        store_bin<CODES, Sink>(bins, mb, d0, min(ge4(x[2], bb), mb.y >> 16));
+        store_bin<CODES, Sink>(bins, mb, d1, min(ge4(x[3], bb), mb.y >> 16));
         return;
     }
     switch ((ma.y >> 8) & 0xffu) {
-    case 1: bin_pair<CODES, 1>(x, ma, mb, bord, bins, d0, d1); break;
-    case 2: bin_pair<CODES, 2>(x, ma, mb, bord, bins, d0, d1); break;
-    case 3: bin_pair<CODES, 3>(x, ma, mb, bord, bins, d0, d1); break;
-    case 4: bin_pair<CODES, 4>(x, ma, mb, bord, bins, d0, d1); break;
-    case 5: bin_pair<CODES, 5>(x, ma, mb, bord, bins, d0, d1); break;
-    case 6: bin_pair<CODES, 6>(x, ma, mb, bord, bins, d0, d1); break;
-    case 7: bin_pair<CODES, 7>(x, ma, mb, bord, bins, d0, d1); break;
-    default: bin_pair<CODES, 8>(x, ma, mb, bord, bins, d0, d1); break;
+    case 1: bin_pair<CODES, 1, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    case 2: bin_pair<CODES, 2, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    case 3: bin_pair<CODES, 3, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    case 4: bin_pair<CODES, 4, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    case 5: bin_pair<CODES, 5, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    case 6: bin_pair<CODES, 6, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    case 7: bin_pair<CODES, 7, Sink>(x, ma, mb, bord, bins, d0, d1); break;
+    default: bin_pair<CODES, 8, Sink>(x, ma, mb, bord, bins, d0, d1); break;
     }
 }
 
@@ -269,9 +283,9 @@ __device__ __forceinline__ void pair_dispatch(const float x[4], const uint4 &ma,
 // factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot.
 // Warp w: factor quad q = w >> 1 (two pairs) for documents 64*(w&1) + lane and
 // + 32: 4 independent search chains per lane per pair.
-template <bool CODES>
+template <bool CODES, class Sink>
 __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
-                                             uint32_t bins, int warp, int lane)
+                                             const Sink &bins, int warp, int lane)
 {
     const int q = warp >> 1;
     const int d0 = ((warp & 1) << 6) | lane, d1 = d0 + 32;
@@ -282,11 +296,11 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
     const float4 v1 = lds_v4f(tile + d1 * 128 + ((q ^ (d1 & 7)) << 4));
     {
         const float x[4] = {v0.x, v1.x, v0.y, v1.y};
-        pair_dispatch<CODES>(x, m0, m1, bord, bins, d0, d1);
+        pair_dispatch<CODES, Sink>(x, m0, m1, bord, bins, d0, d1);
     }
     {
         const float x[4] = {v0.z, v1.z, v0.w, v1.w};
-        pair_dispatch<CODES>(x, m2, m3, bord, bins, d0, d1);
+        pair_dispatch<CODES, Sink>(x, m2, m3, bord, bins, d0, d1);
     }
 }
 
@@ -507,9 +521,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
                 const uint32_t sb = ring + slot * p.slot_bytes;
                 for (int s = 0; s < nsub; ++s)
-                    binarize_sub<MODE == MODE_FUSED>(sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
-                                                     sb + p.off_bord + s * p.bord_stride, bins, warp,
-                                                     lane);
+                    binarize_sub<MODE == MODE_FUSED, SmemSink>(
+                        sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
+                        sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp, lane);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty);
                 if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -636,6 +650,96 @@ __global__ void __launch_bounds__(kConsumerThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K4: small-batch latency path (config c5).  Two launches:
+//  (1) odf_lat_binarize_kernel, grid (n_fchunks, n_tiles): one CTA per 128-doc x
+//      32-factor sub-tile writes its 7-bit code columns to a global [tile][n_cols][128]
+//      block (L2-resident), so binarization of one tile is spread over many SMs;
+//  (2) odf_lat_apply_kernel, grid (S, n_tiles): CTA s applies the tree chunks
+//      [s*C/S, (s+1)*C/S) to its tile and writes a partial [128]; the last CTA of
+//      a tile (atomic ticket) sums the S partials in ascending s -> deterministic.
+// The association differs from the main path (tree ranges per split), so these
+// scores are held to the tolerance, not bit-exactness.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kConsumerThreads)
+    odf_lat_binarize_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
+{
+    if (smem_addr(smem_raw) & 1023u) __trap();
+    const int c = blockIdx.x;
+    const int64_t tile = blockIdx.y;
+    const uint32_t t_off = 0, m_off = kFSubBytes, b_off = kFSubBytes + kMetaBytes;
+    const uint32_t bar = b_off + ((p.bord_stride + 15u) & ~15u);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        const uint2 bc = p.bchunk[c];
+        mbar_expect_tx(bar, kFSubBytes + kMetaBytes + bc.y);
+        tma_load_2d(t_off, &tmap, c * kFSub, static_cast<int>(tile * kTile), bar);
+        bulk_g2s(m_off, p.fmeta + c * kFSub, kMetaBytes, bar);
+        if (bc.y) bulk_g2s(b_off, reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, bar);
+        if (c == 0) p.lat_counter[tile] = 0u;  // ticket for kernel (2), stream-ordered
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    binarize_sub<true, GmemSink>(t_off, m_off, b_off,
+                                 GmemSink{p.lat_codes + tile * static_cast<int64_t>(p.n_cols) * kTile},
+                                 warp, lane);
+}
+
+template <int DEPTH>
+__global__ void __launch_bounds__(kConsumerThreads)
+    odf_lat_apply_kernel(const KParams p)
+{
+    if (smem_addr(smem_raw) & 1023u) __trap();
+    const int split = blockIdx.x, S = gridDim.x;
+    const int64_t tile = blockIdx.y;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bins = 0;
+    const uint32_t cols_bytes = static_cast<uint32_t>(p.n_cols) * kTile;
+    const uint32_t chunk = (cols_bytes + 1023u) & ~1023u;
+    const uint32_t red = chunk + ((p.chunk_bytes + 1023u) & ~1023u);
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.lat_codes + tile * static_cast<int64_t>(cols_bytes));
+        for (uint32_t k = tid; k < cols_bytes / 16; k += kConsumerThreads) sts_v4u(bins + 16 * k, src[k]);
+    }
+    const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
+    const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const uint32_t lane_bins = bins + lane * 4u;
+    for (int c = c_lo; c < c_hi; ++c) {
+        __syncthreads();  // previous chunk consumed (and, first time, codes stored)
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.chunks + static_cast<size_t>(c) * p.chunk_bytes);
+        for (uint32_t k = tid; k < p.chunk_bytes / 16; k += kConsumerThreads)
+            sts_v4u(chunk + 16 * k, __ldg(src + k));
+        __syncthreads();
+        const int64_t rem = p.n_trees - static_cast<int64_t>(c) * p.tc;
+        apply_chunk<DEPTH>(chunk, rem < p.tc ? static_cast<int>(rem) : p.tc, p.desc_bytes,
+                           p.table_stride, lane_bins, warp, acc);
+    }
+    sts_v4f(red + warp * (kTile * 4) + lane * 16, acc[0], acc[1], acc[2], acc[3]);
+    __syncthreads();
+    float *part = p.lat_partial + (tile * S) * kTile;
+    if (tid < kTile) {
+        float v = lds_f32(red + tid * 4);
+#pragma unroll
+        for (int w = 1; w < kConsumerWarps; ++w) v += lds_f32(red + w * (kTile * 4) + tid * 4);
+        part[split * kTile + tid] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ uint32_t last;
+    if (tid == 0) last = (atomicAdd(p.lat_counter + tile, 1u) == static_cast<uint32_t>(S - 1)) ? 1u : 0u;
+    __syncthreads();
+    if (last && tid < kTile) {
+        __threadfence();
+        float v = __ldcg(part + tid);
+        for (int s2 = 1; s2 < S; ++s2) v += __ldcg(part + s2 * kTile + tid);
+        const int64_t doc = tile * kTile + tid;
+        if (doc < p.n_docs) p.scores[doc] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 template <int MODE, int DEPTH>
@@ -673,18 +777,66 @@ static const void *index_kernel(int depth)
     return (depth < 0 || depth > 10) ? nullptr : t[depth];
 }
 
+template <int DEPTH>
+static const void *lat_fn()
+{
+    return reinterpret_cast<const void *>(&odf_lat_apply_kernel<DEPTH>);
+}
+static const void *lat_apply_kernel(int depth)
+{
+    static const void *t[11] = {lat_fn<0>(), lat_fn<1>(), lat_fn<2>(), lat_fn<3>(),
+                                lat_fn<4>(), lat_fn<5>(), lat_fn<6>(), lat_fn<7>(),
+                                lat_fn<8>(), lat_fn<9>(), lat_fn<10>()};
+    return (depth < 0 || depth > 10) ? nullptr : t[depth];
+}
+
+cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,
+                           size_t smem_bin, size_t smem_apply, cudaStream_t s)
+{
+    KParams pc = p;
+    CUtensorMap tm;
+    if (tmap)
+        tm = *tmap;
+    else
+        memset(&tm, 0, sizeof(tm));
+    cudaError_t e = cudaSuccess;
+    if (p.n_fchunks > 0) {
+        void *args[] = {&pc, &tm};
+        e = cudaLaunchKernel(reinterpret_cast<const void *>(&odf_lat_binarize_kernel),
+                             dim3(p.n_fchunks, static_cast<unsigned>(p.n_tiles)), dim3(kConsumerThreads),
+                             args, smem_bin, s);
+        if (e != cudaSuccess) return e;
+    } else {
+        e = cudaMemsetAsync(p.lat_counter, 0, sizeof(uint32_t) * p.n_tiles, s);
+        if (e != cudaSuccess) return e;
+    }
+    void *args2[] = {&pc};
+    return cudaLaunchKernel(lat_apply_kernel(depth), dim3(splits, static_cast<unsigned>(p.n_tiles)),
+                            dim3(kConsumerThreads), args2, smem_apply, s);
+}
+
+static cudaError_t opt_in(const void *f, int max_smem)
+{
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem - static_cast<int>(a.sharedSizeBytes));
+}
+
 cudaError_t prepare_kernels(int max_smem)
 {
     for (int d = 0; d <= 10; ++d) {
         const void *fs[] = {main_kernel(MODE_FUSED, d), main_kernel(MODE_APPLY, d),
-                            index_kernel(d)};
+                            index_kernel(d), lat_apply_kernel(d)};
         for (const void *f : fs) {
-            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+            cudaError_t e = opt_in(f, max_smem);
             if (e != cudaSuccess) return e;
         }
     }
-    return cudaFuncSetAttribute(main_kernel(MODE_BINARIZE, 0),
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
+    if (e != cudaSuccess) return e;
+    return opt_in(main_kernel(MODE_BINARIZE, 0), max_smem);
 }
 
 int occupancy_main(int mode, int depth, size_t smem)

@@ -86,6 +86,10 @@ def lib():
     L.odf_leaf_indices.argtypes = [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]
     L.odf_index_fingerprint.restype = ctypes.c_int
     L.odf_index_fingerprint.argtypes = [_vp, _vp, _i64, _vp, _vp]
+    L.odf_latency_workspace_bytes.restype = ctypes.c_size_t
+    L.odf_latency_workspace_bytes.argtypes = [_vp, _i64, _i32]
+    L.odf_score_latency.restype = ctypes.c_int
+    L.odf_score_latency.argtypes = [_vp, _vp, _i64, _i64, _vp, _i32, _vp, ctypes.c_size_t, _vp]
     L.odf_score_host.restype = ctypes.c_int
     L.odf_score_host.argtypes = [_vp, _vp, _i64, _i64, _vp, _i64, _vp]
     _lib = L
@@ -94,7 +98,8 @@ def lib():
 
 ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_model",
                "odf_get_info", "odf_bins_layout", "odf_binarize", "odf_apply", "odf_score",
-               "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host")
+               "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host",
+               "odf_latency_workspace_bytes", "odf_score_latency")
 
 
 def _check(status: int):
@@ -207,6 +212,21 @@ class Model:
         if out is None:
             out = torch.empty(n, dtype=torch.float32, device=self._dev())
         _check(lib().odf_score(self._h, _ptr(x), n, ld, _ptr(out), _stream(stream, self._dev())))
+        return out
+
+    def latency_workspace(self, max_docs: int, splits: int = 0) -> torch.Tensor:
+        n = int(lib().odf_latency_workspace_bytes(self._h, int(max_docs), int(splits)))
+        return torch.empty(max(n, 256), dtype=torch.uint8, device=self._dev())
+
+    def score_latency(self, x: torch.Tensor, workspace: torch.Tensor, out=None, splits: int = 0,
+                      stream=None):
+        """K4 small-batch path: two launches, tolerance-level parity with score()."""
+        n, ld = self._check_x(x)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=self._dev())
+        _check(lib().odf_score_latency(self._h, _ptr(x), n, ld, _ptr(out), int(splits),
+                                       _ptr(workspace), workspace.numel(),
+                                       _stream(stream, self._dev())))
         return out
 
     def score_host(self, x, out=None, chunk_docs: int = 65536, stream=None):

@@ -267,3 +267,50 @@ def test_c3_full_size():
 
 def test_c4_full_size():
     _sampled_full_size("c4", n_sample=600)
+
+
+# ---------------------------------------------------------------------------
+# K4 latency path (config c5 shape): tolerance parity, determinism
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("batch,splits", [(1, 0), (100, 0), (100, 37), (1000, 0), (5000, 0),
+                                          (777, 1)])
+def test_latency_path(batch, splits):
+    import torch
+    case = synth.make_case("c5", n_docs=12000)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    offs = synth.latency_queries(5, case.n_docs, batch, 3)
+    ws = m.latency_workspace(batch, splits)
+    tol = tolerance(case.leaf_values, case.depth)
+    for o in offs:
+        q = x[o:o + batch]
+        a = m.score_latency(q, ws, splits=splits).cpu().numpy()
+        b = m.score_latency(q, ws, splits=splits).cpu().numpy()
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), "not deterministic"
+        rows = np.arange(o, o + batch)
+        if batch > 300:
+            rows = rows[np.random.default_rng(int(o)).choice(batch, 300, replace=False)]
+        s64 = oracle.score_rows(case.x, rows, case.feature_index, case.thresholds,
+                                case.leaf_values, case.depth)
+        err = np.abs(a[rows - o].astype(np.float64) - s64)
+        assert err.max() <= tol, (err.max(), tol)
+        fused = m.score(q).cpu().numpy()
+        assert np.abs(fused.astype(np.float64) - a).max() <= 2 * tol
+    torch.cuda.synchronize()
+    m.close()
+
+
+def test_latency_path_depth10_and_small_workspace_error():
+    import torch
+    from paper_2205_07307_b200 import OdfError
+    case = synth.tiny_case(seed=71, n_docs=300, n_features=20, n_trees=40, depth=10, pool=30)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    ws = m.latency_workspace(300)
+    got = m.score_latency(x, ws).cpu().numpy()
+    s64, _ = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, 10)
+    assert np.abs(got - s64).max() <= tolerance(case.leaf_values, 10)
+    with pytest.raises(OdfError):
+        m.score_latency(x, ws[:16])
+    torch.cuda.synchronize()
+    m.close()
