@@ -111,7 +111,7 @@ def main():
             worst = max(worst, float(np.abs(got[rows - o] - s64).max()))
         entry["parity"] = {"checked_queries": int(min(len(pick), 20)),
                            "sample": "seeded 1% of queries, <=20 checked, <=200 docs each",
-                           "max_abs_err": worst, "tolerance": tol, "ok": worst <= tol}
+                           "max_abs_err": worst, "tolerance": tol, "ok": bool(worst <= tol)}
         res["batches"][str(B)] = entry
     print(json.dumps(res), flush=True)
     m.close()
