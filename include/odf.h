@@ -86,6 +86,26 @@ ODF_API odf_status odf_load_model(const int32_t *feature_index, const float *thr
                           const float *leaf_values, int32_t depth, int64_t n_trees,
                           int32_t n_features, int device, odf_model **out);
 
+/* General load (fp32 or MatrixNet integer leaves).  leaf_type ODF_LEAF_U32:
+ * leaf_values is uint32 [n_trees << depth]; scores are the paper's u64 sums R
+ * and (R - 2^31) * S + B with S = scale, B = bias (applied once
+ * per document, SURVEY 8(c) reading 9), computed by odf_score_u64 /
+ * odf_apply_u64 (exact: zero-tolerance parity).  Other fields as odf_load_model. */
+#define ODF_LEAF_F32 0
+#define ODF_LEAF_U32 1
+typedef struct {
+    const int32_t *feature_index; /* [n_trees*depth] */
+    const float *thresholds;      /* [n_trees*depth] */
+    const void *leaf_values;      /* [n_trees << depth], float or uint32 per leaf_type */
+    int32_t leaf_type;            /* ODF_LEAF_F32 / ODF_LEAF_U32 */
+    int32_t depth;
+    int64_t n_trees;
+    int32_t n_features;
+    int32_t device;
+    double scale, bias;           /* integer mode only */
+} odf_model_desc;
+ODF_API odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out);
+
 ODF_API void odf_free_model(odf_model *m); /* NULL is a no-op; synchronises the device */
 
 typedef struct {
@@ -99,6 +119,7 @@ typedef struct {
     int32_t stages_fused;       /* ring stages of the fused kernel */
     int32_t smem_fused;         /* dynamic shared memory per CTA of the fused kernel, bytes */
     int32_t num_sms;
+    int32_t leaf_type;          /* ODF_LEAF_F32 / ODF_LEAF_U32 */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);
@@ -129,6 +150,16 @@ ODF_API odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t 
  * summation order); bins live only in shared memory, never in HBM.           */
 ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
                      float *d_scores, void *stream);
+
+/* Integer-leaf models (ODF_LEAF_U32): fused (from factors) and stage-2 (from
+ * bins) scoring into d_sums [n_docs] uint64 (R, exact) and/or d_scores [n_docs]
+ * double ((R - 2^31) * S + B, each operation rounded to nearest, no FMA); either
+ * output may be NULL but not both.  fp32 models are rejected (ODF_E_INVALID_ARG),
+ * and odf_score / odf_apply reject integer models.                           */
+ODF_API odf_status odf_score_u64(const odf_model *m, const float *d_factors, int64_t n_docs,
+                                 int64_t ld, uint64_t *d_sums, double *d_scores, void *stream);
+ODF_API odf_status odf_apply_u64(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                                 uint64_t *d_sums, double *d_scores, void *stream);
 
 /* Test/debug (K6): leaf indices idx[d][t] (true index, level l = bit l) of
  * documents [doc0, doc0+ndoc) and trees [tree0, tree0+ntree) from d_bins

@@ -91,6 +91,8 @@ struct odf_model {
     uint8_t *d_chunks = nullptr;
     uint2 *d_splits = nullptr;
     uint2 *d_bchunk = nullptr;
+    bool leaf_u32 = false;
+    double scale = 1.0, bias = 0.0;
     Plan fused, binz, apply;
     // odf_score_host staging
     std::mutex host_mu;
@@ -110,7 +112,8 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
 {
     const uint32_t cols = (mode == MODE_BINARIZE) ? m.n_used : m.n_cols;
     const uint32_t bins = align_up(static_cast<uint64_t>(cols) * kTile, 1024);
-    const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, kRedBytes);
+    const uint32_t red_bytes = m.leaf_u32 ? 2 * kRedBytes : kRedBytes;
+    const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes);
     const uint32_t bars = align_up(16u * 8 + 16 + 8u * m.n_fchunks, 128);  // + bchunk copy
     // a factor sub-tile travels as [16 KB box][512 B fmeta][its border arrays]
     const uint32_t unit = kFSubBytes + kMetaBytes + m.bord_stride;
@@ -203,6 +206,9 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.slot_bytes = pl.slot_bytes;
     p.stages = pl.stages;
     p.fsub_per_job = pl.fsub;
+    p.leaf_u32 = m->leaf_u32 ? 1 : 0;
+    p.scale = m->scale;
+    p.bias = m->bias;
     p.off_meta = pl.off_meta;
     p.off_bord = pl.off_bord;
     p.bord_stride = m->bord_stride;
@@ -264,8 +270,40 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
                           const float *leaf_values, int32_t depth, int64_t n_trees,
                           int32_t n_features, int device, odf_model **out)
 {
+    odf_model_desc d;
+    memset(&d, 0, sizeof d);
+    d.feature_index = feature_index;
+    d.thresholds = thresholds;
+    d.leaf_values = leaf_values;
+    d.leaf_type = ODF_LEAF_F32;
+    d.depth = depth;
+    d.n_trees = n_trees;
+    d.n_features = n_features;
+    d.device = device;
+    d.scale = 1.0;
+    d.bias = 0.0;
+    return odf_load_model_ex(&d, out);
+}
+
+odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
+{
     if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
+    if (!desc) return fail(ODF_E_INVALID_ARG, "desc is NULL");
+    const int32_t *feature_index = desc->feature_index;
+    const float *thresholds = desc->thresholds;
+    const int32_t depth = desc->depth;
+    const int64_t n_trees = desc->n_trees;
+    const int32_t n_features = desc->n_features;
+    const int device = desc->device;
+    const bool u32 = desc->leaf_type == ODF_LEAF_U32;
+    if (desc->leaf_type != ODF_LEAF_F32 && !u32)
+        return fail(ODF_E_INVALID_ARG, "leaf_type %d unknown", desc->leaf_type);
+    const float *leaf_f = static_cast<const float *>(desc->leaf_values);
+    const uint32_t *leaf_u = static_cast<const uint32_t *>(desc->leaf_values);
+    const void *leaf_values = desc->leaf_values;
+    if (u32 && (!std::isfinite(desc->scale) || !std::isfinite(desc->bias)))
+        return fail(ODF_E_INVALID_ARG, "scale / bias not finite");
     if (depth < 0 || depth > ODF_MAX_DEPTH) return fail(ODF_E_INVALID_ARG, "depth %d not in [0, %d]", depth, ODF_MAX_DEPTH);
     if (n_trees < 0) return fail(ODF_E_INVALID_ARG, "n_trees < 0");
     if (n_trees > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
@@ -282,9 +320,10 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
         if (!std::isfinite(thresholds[k]))
             return fail(ODF_E_INVALID_ARG, "thresholds[%lld] is not finite", (long long)k);
     }
-    for (int64_t k = 0; k < n_leaves; ++k)
-        if (!std::isfinite(leaf_values[k]))
-            return fail(ODF_E_INVALID_ARG, "leaf_values[%lld] is not finite", (long long)k);
+    if (!u32)
+        for (int64_t k = 0; k < n_leaves; ++k)
+            if (!std::isfinite(leaf_f[k]))
+                return fail(ODF_E_INVALID_ARG, "leaf_values[%lld] is not finite", (long long)k);
 
     int n_dev = 0;
     if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
@@ -296,6 +335,9 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
     m->depth = depth;
     m->n_trees = n_trees;
     m->n_features = n_features;
+    m->leaf_u32 = u32;
+    m->scale = desc->scale;
+    m->bias = desc->bias;
 
     // ---- borders per factor (sorted, unique by ==) ----
     std::vector<std::vector<float>> borders(n_features);
@@ -425,7 +467,12 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
             desc[2 * l + 1] = (128u - K) * 0x01010101u;
         }
         float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
-        for (uint32_t F = 0; F < nleaf; ++F) tab[F] = leaf_values[t * nleaf + (nleaf - 1 - F)];
+        if (u32) {
+            uint32_t *tab_u = reinterpret_cast<uint32_t *>(tab);
+            for (uint32_t F = 0; F < nleaf; ++F) tab_u[F] = leaf_u[t * nleaf + (nleaf - 1 - F)];
+        } else {
+            for (uint32_t F = 0; F < nleaf; ++F) tab[F] = leaf_f[t * nleaf + (nleaf - 1 - F)];
+        }
     }
 
     // ---- device ----
@@ -495,6 +542,7 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->stages_fused = m->fused.stages;
     info->smem_fused = static_cast<int32_t>(m->fused.smem);
     info->num_sms = m->num_sms;
+    info->leaf_type = m->leaf_u32 ? ODF_LEAF_U32 : ODF_LEAF_F32;
     return ok();
 }
 
@@ -511,7 +559,8 @@ odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
 }
 
 static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64_t n_docs, int64_t ld,
-                           const uint8_t *bins_in, uint8_t *bins_out, float *scores, cudaStream_t s)
+                           const uint8_t *bins_in, uint8_t *bins_out, float *scores, cudaStream_t s,
+                           uint64_t *sums = nullptr, double *dscores = nullptr)
 {
     const Plan &pl = mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
     KParams p = base_params(m, pl);
@@ -520,6 +569,8 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     p.bins_in = bins_in;
     p.bins_out = bins_out;
     p.scores = scores;
+    p.sums = reinterpret_cast<unsigned long long *>(sums);
+    p.dscores = dscores;
     CUtensorMap tm;
     const CUtensorMap *tmp = nullptr;
     if (mode != MODE_APPLY && p.n_fchunks > 0) {
@@ -552,6 +603,7 @@ odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, 
                      void *stream)
 {
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "integer-leaf model: use odf_apply_u64");
     if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
@@ -566,12 +618,41 @@ odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs,
                      float *d_scores, void *stream)
 {
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "integer-leaf model: use odf_score_u64");
     odf_status st = check_factors(m, d_factors, n_docs, ld);
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
     return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, d_scores,
                     static_cast<cudaStream_t>(stream));
+}
+
+odf_status odf_score_u64(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                         uint64_t *d_sums, double *d_scores, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (!m->leaf_u32) return fail(ODF_E_INVALID_ARG, "fp32-leaf model: use odf_score");
+    odf_status st = check_factors(m, d_factors, n_docs, ld);
+    if (st != ODF_OK) return st;
+    if (n_docs == 0) return ok();
+    if (!d_sums && !d_scores) return fail(ODF_E_INVALID_ARG, "d_sums and d_scores are both NULL");
+    return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, nullptr,
+                    static_cast<cudaStream_t>(stream), d_sums, d_scores);
+}
+
+odf_status odf_apply_u64(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, uint64_t *d_sums,
+                         double *d_scores, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (!m->leaf_u32) return fail(ODF_E_INVALID_ARG, "fp32-leaf model: use odf_apply");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs == 0) return ok();
+    if (!d_sums && !d_scores) return fail(ODF_E_INVALID_ARG, "d_sums and d_scores are both NULL");
+    if (m->n_used > 0 && !d_bins) return fail(ODF_E_INVALID_ARG, "d_bins is NULL");
+    if (reinterpret_cast<uintptr_t>(d_bins) % 16 != 0)
+        return fail(ODF_E_INVALID_ARG, "d_bins not 16-byte aligned");
+    return run_main(m, MODE_APPLY, nullptr, n_docs, 0, d_bins, nullptr, nullptr,
+                    static_cast<cudaStream_t>(stream), d_sums, d_scores);
 }
 
 static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, bool fp,
@@ -661,6 +742,7 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
                              size_t workspace_bytes, void *stream)
 {
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_UNSUPPORTED, "latency path: fp32-leaf models only");
     odf_status st = check_factors(m, d_factors, n_docs, ld);
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
@@ -750,6 +832,7 @@ odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, 
         if ((e = cudaMemcpyAsync(m->d_stage[b], h_factors + d0 * ld, static_cast<size_t>(n) * ld * 4,
                                  cudaMemcpyHostToDevice, s)) != cudaSuccess)
             return cuda_fail(e, "H2D");
+        if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "odf_score_host: fp32-leaf models only");
         odf_status st = odf_score(m, m->d_stage[b], n, ld, m->d_sstage[b], s);
         if (st != ODF_OK) return st;
         if ((e = cudaMemcpyAsync(h_scores + d0, m->d_sstage[b], static_cast<size_t>(n) * 4,

@@ -45,6 +45,11 @@ struct KParams {
     const uint8_t *bins_in;  // blocked bins (apply / index kernels)
     uint8_t *bins_out;       // blocked bins (binarize)
     float *scores;
+    // ---- MatrixNet integer mode: u32 leaves, u64 sums ----
+    int32_t leaf_u32;        // 1: leaf tables hold u32 answers
+    double scale, bias;      // final (R - 2^31) * S + B
+    unsigned long long *sums;  // [n_docs] u64 sums R (may be null)
+    double *dscores;         // [n_docs] final scores (may be null)
     // ---- shared-memory plan (byte offsets from the 1 KB aligned base) ----
     uint32_t off_bins, off_ring, off_red, off_bars;
     uint32_t slot_bytes;

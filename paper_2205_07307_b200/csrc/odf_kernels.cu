@@ -390,10 +390,38 @@ __device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint3
 
 __host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 1) & ~1) * 8; }
 
-template <int DEPTH>
+// Per-lane accumulators of the 4 documents: fp32 leaves summed in fp32 (the
+// north_star's path) or, for MatrixNet integer models, u32 leaves summed in u64
+// (exact, order-free).
+template <bool U32>
+struct Acc;
+template <>
+struct Acc<false> {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    __device__ __forceinline__ void add(int n, uint32_t addr) { v[n] += lds_f32(addr); }
+    static constexpr uint32_t kRed = kRedBytes;
+    __device__ __forceinline__ void to_red(uint32_t red, int warp, int lane) const
+    {
+        sts_v4f(red + warp * (kTile * 4) + lane * 16, v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct Acc<true> {
+    unsigned long long v[4] = {0ull, 0ull, 0ull, 0ull};
+    __device__ __forceinline__ void add(int n, uint32_t addr) { v[n] += lds_u32(addr); }
+    static constexpr uint32_t kRed = 2 * kRedBytes;
+    __device__ __forceinline__ void to_red(uint32_t red, int warp, int lane) const
+    {
+        const uint32_t a = red + warp * (kTile * 8) + lane * 32;
+        sst<ulonglong2>(a, make_ulonglong2(v[0], v[1]));
+        sst<ulonglong2>(a + 16, make_ulonglong2(v[2], v[3]));
+    }
+};
+
+template <int DEPTH, bool U32>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, int n_in, uint32_t desc_bytes,
                                             uint32_t stride, uint32_t lane_bins, int warp,
-                                            float acc[4])
+                                            Acc<U32> &acc)
 {
 #pragma unroll 2
     for (int i = warp; i < n_in; i += kConsumerWarps) {
@@ -402,7 +430,31 @@ __device__ __forceinline__ void apply_chunk(uint32_t chunk, int n_in, uint32_t d
         uint32_t a[4];
         leaf_addrs<DEPTH>(d, lane_bins, tb, a);
 #pragma unroll
-        for (int n = 0; n < 4; ++n) acc[n] += lds_f32(a[n]);
+        for (int n = 0; n < 4; ++n) acc.add(n, a[n]);
+    }
+}
+
+// Fixed-order combine of the 16 warp partials of document tid (< 128) and store.
+__device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int tid, int64_t doc,
+                                           Acc<false> *)
+{
+    float s = lds_f32(red + tid * 4);
+#pragma unroll
+    for (int w = 1; w < kConsumerWarps; ++w) s += lds_f32(red + w * (kTile * 4) + tid * 4);
+    if (doc < p.n_docs) p.scores[doc] = s;
+}
+__device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int tid, int64_t doc,
+                                           Acc<true> *)
+{
+    unsigned long long r = 0;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) r += sld<unsigned long long>(red + w * (kTile * 8) + tid * 8);
+    if (doc < p.n_docs) {
+        if (p.sums) p.sums[doc] = r;
+        // (R - 2^31) * S + B, rounded op by op (no FMA contraction)
+        if (p.dscores)
+            p.dscores[doc] = __dadd_rn(__dmul_rn(__dsub_rn(static_cast<double>(r), 2147483648.0), p.scale),
+                                       p.bias);
     }
 }
 
@@ -422,7 +474,7 @@ __device__ __forceinline__ void expand_splits(const KParams &p, uint32_t bins, i
 // ---------------------------------------------------------------------------
 // Main persistent kernel: MODE_FUSED (K3), MODE_BINARIZE (K1), MODE_APPLY (K2)
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH>
+template <int MODE, int DEPTH, bool U32>
 __global__ void __launch_bounds__(kThreads, 1)
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -543,29 +595,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_consumers();  // all bins of the tile written
 
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        Acc<U32> acc;
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
             mbar_wait(full, ph);
             const int64_t rem = p.n_trees - static_cast<int64_t>(c) * p.tc;
             const int n_in = rem < p.tc ? static_cast<int>(rem) : p.tc;
-            apply_chunk<DEPTH>(ring + slot * p.slot_bytes, n_in, p.desc_bytes, p.table_stride,
-                               lane_bins, warp, acc);
+            apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, n_in, p.desc_bytes,
+                                    p.table_stride, lane_bins, warp, acc);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty);
             if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
         }
         // reduction buffer aliases the bins: wait until every warp is done with them
         named_bar_consumers();
-        sts_v4f(red + warp * (kTile * 4) + lane * 16, acc[0], acc[1], acc[2], acc[3]);
+        acc.to_red(red, warp, lane);
         named_bar_consumers();
-        if (tid < kTile) {
-            float s = lds_f32(red + tid * 4);
-#pragma unroll
-            for (int w = 1; w < kConsumerWarps; ++w) s += lds_f32(red + w * (kTile * 4) + tid * 4);
-            const int64_t doc = tile * kTile + tid;
-            if (doc < p.n_docs) p.scores[doc] = s;
-        }
+        if (tid < kTile) finish_doc(p, red, tid, tile * kTile + tid, static_cast<Acc<U32> *>(nullptr));
         if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
             fence_proxy_async();  // generic writes to the bins region precede the next TMA
         }
@@ -704,7 +750,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
     const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    Acc<false> acc;
     const uint32_t lane_bins = bins + lane * 4u;
     for (int c = c_lo; c < c_hi; ++c) {
         __syncthreads();  // previous chunk consumed (and, first time, codes stored)
@@ -713,10 +759,10 @@ __global__ void __launch_bounds__(kConsumerThreads)
             sts_v4u(chunk + 16 * k, __ldg(src + k));
         __syncthreads();
         const int64_t rem = p.n_trees - static_cast<int64_t>(c) * p.tc;
-        apply_chunk<DEPTH>(chunk, rem < p.tc ? static_cast<int>(rem) : p.tc, p.desc_bytes,
-                           p.table_stride, lane_bins, warp, acc);
+        apply_chunk<DEPTH, false>(chunk, rem < p.tc ? static_cast<int>(rem) : p.tc, p.desc_bytes,
+                                  p.table_stride, lane_bins, warp, acc);
     }
-    sts_v4f(red + warp * (kTile * 4) + lane * 16, acc[0], acc[1], acc[2], acc[3]);
+    acc.to_red(red, warp, lane);
     __syncthreads();
     float *part = p.lat_partial + (tile * S) * kTile;
     if (tid < kTile) {
@@ -742,25 +788,27 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH>
+template <int MODE, int DEPTH, bool U32>
 static const void *main_fn()
 {
-    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH>);
+    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH, U32>);
 }
 
-#define ODF_DEPTH_TABLE(M)                                                                 \
-    {main_fn<M, 0>(), main_fn<M, 1>(), main_fn<M, 2>(), main_fn<M, 3>(), main_fn<M, 4>(),   \
-     main_fn<M, 5>(), main_fn<M, 6>(), main_fn<M, 7>(), main_fn<M, 8>(), main_fn<M, 9>(),   \
-     main_fn<M, 10>()}
+#define ODF_DEPTH_TABLE(M, U)                                                              \
+    {main_fn<M, 0, U>(), main_fn<M, 1, U>(), main_fn<M, 2, U>(), main_fn<M, 3, U>(),       \
+     main_fn<M, 4, U>(), main_fn<M, 5, U>(), main_fn<M, 6, U>(), main_fn<M, 7, U>(),       \
+     main_fn<M, 8, U>(), main_fn<M, 9, U>(), main_fn<M, 10, U>()}
 
-static const void *main_kernel(int mode, int depth)
+static const void *main_kernel(int mode, int depth, bool u32 = false)
 {
-    static const void *fused[11] = ODF_DEPTH_TABLE(MODE_FUSED);
-    static const void *apply[11] = ODF_DEPTH_TABLE(MODE_APPLY);
-    static const void *binz = main_fn<MODE_BINARIZE, 0>();
+    static const void *fused[2][11] = {ODF_DEPTH_TABLE(MODE_FUSED, false),
+                                       ODF_DEPTH_TABLE(MODE_FUSED, true)};
+    static const void *apply[2][11] = {ODF_DEPTH_TABLE(MODE_APPLY, false),
+                                       ODF_DEPTH_TABLE(MODE_APPLY, true)};
+    static const void *binz = main_fn<MODE_BINARIZE, 0, false>();
     if (depth < 0 || depth > 10) return nullptr;
-    if (mode == MODE_FUSED) return fused[depth];
-    if (mode == MODE_APPLY) return apply[depth];
+    if (mode == MODE_FUSED) return fused[u32 ? 1 : 0][depth];
+    if (mode == MODE_APPLY) return apply[u32 ? 1 : 0][depth];
     return binz;
 }
 
@@ -828,6 +876,7 @@ cudaError_t prepare_kernels(int max_smem)
 {
     for (int d = 0; d <= 10; ++d) {
         const void *fs[] = {main_kernel(MODE_FUSED, d), main_kernel(MODE_APPLY, d),
+                            main_kernel(MODE_FUSED, d, true), main_kernel(MODE_APPLY, d, true),
                             index_kernel(d), lat_apply_kernel(d)};
         for (const void *f : fs) {
             cudaError_t e = opt_in(f, max_smem);
@@ -851,7 +900,7 @@ int occupancy_main(int mode, int depth, size_t smem)
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s)
 {
-    const void *f = main_kernel(mode, depth);
+    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0);
     if (!f) return cudaErrorInvalidValue;
     KParams pc = p;
     CUtensorMap tm;

@@ -38,7 +38,16 @@ class _Info(ctypes.Structure):
                 ("chunk_bytes", ctypes.c_int64), ("model_device_bytes", ctypes.c_int64),
                 ("max_borders", ctypes.c_int32), ("total_borders", ctypes.c_int64),
                 ("borders_in_smem", ctypes.c_int32), ("stages_fused", ctypes.c_int32),
-                ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32)]
+                ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32),
+                ("leaf_type", ctypes.c_int32)]
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("feature_index", ctypes.c_void_p), ("thresholds", ctypes.c_void_p),
+                ("leaf_values", ctypes.c_void_p), ("leaf_type", ctypes.c_int32),
+                ("depth", ctypes.c_int32), ("n_trees", ctypes.c_int64),
+                ("n_features", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("scale", ctypes.c_double), ("bias", ctypes.c_double)]
 
 
 _lib = None
@@ -69,6 +78,12 @@ def lib():
     L.odf_load_model.restype = ctypes.c_int
     L.odf_load_model.argtypes = [_vp, _vp, _vp, _i32, _i64, _i32, ctypes.c_int,
                                  ctypes.POINTER(_vp)]
+    L.odf_load_model_ex.restype = ctypes.c_int
+    L.odf_load_model_ex.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(_vp)]
+    L.odf_score_u64.restype = ctypes.c_int
+    L.odf_score_u64.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp]
+    L.odf_apply_u64.restype = ctypes.c_int
+    L.odf_apply_u64.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp]
     L.odf_free_model.restype = None
     L.odf_free_model.argtypes = [_vp]
     L.odf_get_info.restype = ctypes.c_int
@@ -99,7 +114,8 @@ def lib():
 ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_model",
                "odf_get_info", "odf_bins_layout", "odf_binarize", "odf_apply", "odf_score",
                "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host",
-               "odf_latency_workspace_bytes", "odf_score_latency")
+               "odf_latency_workspace_bytes", "odf_score_latency", "odf_load_model_ex",
+               "odf_score_u64", "odf_apply_u64")
 
 
 def _check(status: int):
@@ -128,22 +144,24 @@ class Model:
     """An oblivious forest loaded onto one GPU (odf_load_model)."""
 
     def __init__(self, feature_index, thresholds, leaf_values, depth: int, n_features: int,
-                 device: int = 0):
+                 device: int = 0, leaf_type: str = "f32", scale: float = 1.0, bias: float = 0.0):
         L = lib()
         fi = np.ascontiguousarray(feature_index, dtype=np.int32)
         thr = np.ascontiguousarray(thresholds, dtype=np.float32)
-        lv = np.ascontiguousarray(leaf_values, dtype=np.float32)
+        u32 = leaf_type == "u32"
+        lv = np.ascontiguousarray(leaf_values, dtype=np.uint32 if u32 else np.float32)
         depth = int(depth)
         n_trees = lv.size >> depth if depth >= 0 else 0
         if depth >= 0 and (fi.size != n_trees * depth or thr.size != n_trees * depth
                            or lv.size != n_trees << depth):
             raise OdfError(1, f"array sizes {fi.size}/{thr.size}/{lv.size} inconsistent with "
                               f"depth {depth}")
+        d = _Desc(fi.ctypes.data if fi.size else None, thr.ctypes.data if thr.size else None,
+                  lv.ctypes.data if lv.size else None, 1 if u32 else 0, depth, n_trees,
+                  int(n_features), int(device), float(scale), float(bias))
         h = _vp()
-        _check(L.odf_load_model(fi.ctypes.data if fi.size else None,
-                                thr.ctypes.data if thr.size else None,
-                                lv.ctypes.data if lv.size else None,
-                                depth, n_trees, int(n_features), int(device), ctypes.byref(h)))
+        _check(L.odf_load_model_ex(ctypes.byref(d), ctypes.byref(h)))
+        self.leaf_type = "u32" if u32 else "f32"
         self._h = h
         self.device = int(device)
         self.depth = depth
@@ -228,6 +246,22 @@ class Model:
                                        _ptr(workspace), workspace.numel(),
                                        _stream(stream, self._dev())))
         return out
+
+    def score_u64(self, x: torch.Tensor, stream=None):
+        """Integer-leaf model: (u64 sums R as int64 bits, (R - 2^31)*S + B as float64)."""
+        n, ld = self._check_x(x)
+        sums = torch.empty(n, dtype=torch.int64, device=self._dev())
+        sc = torch.empty(n, dtype=torch.float64, device=self._dev())
+        _check(lib().odf_score_u64(self._h, _ptr(x), n, ld, _ptr(sums), _ptr(sc),
+                                   _stream(stream, self._dev())))
+        return sums, sc
+
+    def apply_u64(self, bins: torch.Tensor, n_docs: int, stream=None):
+        sums = torch.empty(int(n_docs), dtype=torch.int64, device=self._dev())
+        sc = torch.empty(int(n_docs), dtype=torch.float64, device=self._dev())
+        _check(lib().odf_apply_u64(self._h, _ptr(bins), int(n_docs), _ptr(sums), _ptr(sc),
+                                   _stream(stream, self._dev())))
+        return sums, sc
 
     def score_host(self, x, out=None, chunk_docs: int = 65536, stream=None):
         """End-to-end from host memory (numpy array or CPU tensor, ideally pinned)."""

@@ -314,3 +314,35 @@ def test_latency_path_depth10_and_small_workspace_error():
         m.score_latency(x, ws[:16])
     torch.cuda.synchronize()
     m.close()
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: MatrixNet integer leaves (u32 answers, u64 sums, (R - 2^31) S + B), zero tolerance
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("depth,n_docs,n_trees", [(6, 1000, 300), (3, 129, 1000), (10, 257, 40),
+                                                  (0, 50, 7)])
+def test_integer_leaves_exact(depth, n_docs, n_trees):
+    import torch
+    from paper_2205_07307_b200 import Model
+    case = synth.tiny_case(seed=400 + depth, n_docs=n_docs, n_features=28, n_trees=n_trees,
+                           depth=depth, pool=20)
+    rng = np.random.default_rng(depth)
+    lv = rng.integers(0, 2 ** 32, n_trees << depth, dtype=np.uint64).astype(np.uint32)
+    S, B = 0.5 ** 20, -3.25
+    m = Model(case.feature_index, case.thresholds, lv, depth, case.n_features, leaf_type="u32",
+              scale=S, bias=B)
+    x = to_dev(case.x)
+    sums, sc = m.score_u64(x)
+    bins = m.binarize(x)
+    sums2, sc2 = m.apply_u64(bins, n_docs)
+    want = oracle.score_u64(case.x, case.feature_index, case.thresholds, lv, depth)
+    got = sums.cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, want)
+    assert np.array_equal(sums2.cpu().numpy().view(np.uint64), want)
+    fin = oracle.finalize(want, S, B)
+    assert np.array_equal(sc.cpu().numpy(), fin) and np.array_equal(sc2.cpu().numpy(), fin)
+    from paper_2205_07307_b200 import OdfError
+    with pytest.raises(OdfError):
+        m.score(x)
+    torch.cuda.synchronize()
+    m.close()
