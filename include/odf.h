@@ -106,6 +106,32 @@ typedef struct {
 } odf_model_desc;
 ODF_API odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out);
 
+/* Paper-native model import (NEXT-2).  The model of §5.1/§6.1:
+ * binary-feature descriptor groups (factor index, number of binary features; the
+ * group's binary features are consecutive), one threshold per binary
+ * feature, STC[h] = number of trees of height h (0..8), per-tree condition
+ * indices into the binary features with trees stored in descending height
+ * (P:307), u32 answers, and S, B of P:309.  The import builds a uniform-depth
+ * integer model of depth D = the largest height present: a tree of height h < D
+ * keeps its h conditions as levels 0..h-1, repeats its level 0 on levels h..D-1,
+ * and its table is replicated (answer j = answer[j mod 2^h]), so those levels
+ * cannot change its answer (height-0 trees: constant answer).  Score with
+ * odf_score_u64 / odf_apply_u64 (exact).  Errors: ODF_E_INVALID_ARG for
+ * out-of-range indices, heights > ODF_MAX_DEPTH, non-finite thresholds, sizes. */
+typedef struct {
+    int32_t n_features;
+    const int32_t *group_factor; /* [n_groups] */
+    const int32_t *group_count;  /* [n_groups], >= 1 */
+    int32_t n_groups;
+    const float *thresholds;     /* [sum group_count] */
+    const int32_t *stc;          /* [ODF_MAX_DEPTH + 1] trees per height 0..10 */
+    const uint32_t *cond_indices; /* [sum_h h * stc[h]] */
+    const uint32_t *leaves;      /* [sum_h 2^h * stc[h]] */
+    double scale, bias;
+    int32_t device;
+} odf_paper_model_desc;
+ODF_API odf_status odf_load_model_paper(const odf_paper_model_desc *desc, odf_model **out);
+
 ODF_API void odf_free_model(odf_model *m); /* NULL is a no-op; synchronises the device */
 
 typedef struct {

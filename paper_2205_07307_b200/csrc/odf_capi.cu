@@ -285,6 +285,86 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
     return odf_load_model_ex(&d, out);
 }
 
+odf_status odf_load_model_paper(const odf_paper_model_desc *d, odf_model **out)
+{
+    if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!d) return fail(ODF_E_INVALID_ARG, "desc is NULL");
+    if (d->n_features < 1) return fail(ODF_E_INVALID_ARG, "n_features < 1");
+    if (d->n_groups < 0 || (d->n_groups > 0 && (!d->group_factor || !d->group_count)))
+        return fail(ODF_E_INVALID_ARG, "bad descriptor groups");
+    // binary feature k -> factor (groups of consecutive binary features)
+    std::vector<int32_t> bf_factor;
+    for (int32_t g = 0; g < d->n_groups; ++g) {
+        if (d->group_factor[g] < 0 || d->group_factor[g] >= d->n_features)
+            return fail(ODF_E_INVALID_ARG, "group_factor[%d] = %d not in [0, %d)", g,
+                        d->group_factor[g], d->n_features);
+        if (d->group_count[g] < 1) return fail(ODF_E_INVALID_ARG, "group_count[%d] < 1", g);
+        bf_factor.insert(bf_factor.end(), d->group_count[g], d->group_factor[g]);
+    }
+    const int64_t K = static_cast<int64_t>(bf_factor.size());
+    if (K > 0 && !d->thresholds) return fail(ODF_E_INVALID_ARG, "thresholds is NULL");
+    if (!d->stc) return fail(ODF_E_INVALID_ARG, "stc is NULL");
+    int32_t D = 0;
+    int64_t T = 0, n_cond = 0, n_leaf = 0;
+    for (int h = 0; h <= ODF_MAX_DEPTH; ++h) {
+        if (d->stc[h] < 0) return fail(ODF_E_INVALID_ARG, "stc[%d] < 0", h);
+        if (d->stc[h] > 0) D = h;
+        T += d->stc[h];
+        n_cond += static_cast<int64_t>(h) * d->stc[h];
+        n_leaf += (int64_t(1) << h) * d->stc[h];
+    }
+    if (n_cond > 0 && !d->cond_indices) return fail(ODF_E_INVALID_ARG, "cond_indices is NULL");
+    if (n_leaf > 0 && !d->leaves) return fail(ODF_E_INVALID_ARG, "leaves is NULL");
+    std::vector<int32_t> fi(static_cast<size_t>(T) * D);
+    std::vector<float> thr(static_cast<size_t>(T) * D);
+    std::vector<uint32_t> lv(static_cast<size_t>(T) << D);
+    // a condition for height-0 trees (never affects the answer): any existing one
+    int32_t f0 = 0;
+    float th0 = 0.0f;
+    if (n_cond > 0) {
+        const uint32_t k = d->cond_indices[0];
+        if (k >= static_cast<uint64_t>(K)) return fail(ODF_E_INVALID_ARG, "cond_indices[0] >= K");
+        f0 = bf_factor[k];
+        th0 = d->thresholds[k];
+    }
+    int64_t t = 0, cb = 0, lb = 0;
+    for (int h = ODF_MAX_DEPTH; h >= 0; --h)  // "trees in descending height"
+        for (int32_t i = 0; i < d->stc[h]; ++i, ++t) {
+            for (int l = 0; l < D; ++l) {
+                int32_t f = f0;
+                float th = th0;
+                if (h > 0) {
+                    const uint32_t k = d->cond_indices[cb + (l < h ? l : 0)];
+                    if (k >= static_cast<uint64_t>(K))
+                        return fail(ODF_E_INVALID_ARG, "cond_indices[%lld] = %u >= K = %lld",
+                                    (long long)(cb + l), k, (long long)K);
+                    f = bf_factor[k];
+                    th = d->thresholds[k];
+                }
+                fi[t * D + l] = f;
+                thr[t * D + l] = th;
+            }
+            for (int64_t j = 0; j < (int64_t(1) << D); ++j)
+                lv[(t << D) + j] = d->leaves[lb + (j & ((int64_t(1) << h) - 1))];
+            cb += h;
+            lb += int64_t(1) << h;
+        }
+    odf_model_desc md;
+    memset(&md, 0, sizeof md);
+    md.feature_index = fi.data();
+    md.thresholds = thr.data();
+    md.leaf_values = lv.data();
+    md.leaf_type = ODF_LEAF_U32;
+    md.depth = D;
+    md.n_trees = T;
+    md.n_features = d->n_features;
+    md.device = d->device;
+    md.scale = d->scale;
+    md.bias = d->bias;
+    return odf_load_model_ex(&md, out);
+}
+
 odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
 {
     if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");

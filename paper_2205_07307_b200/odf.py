@@ -50,6 +50,15 @@ class _Desc(ctypes.Structure):
                 ("scale", ctypes.c_double), ("bias", ctypes.c_double)]
 
 
+class _PaperDesc(ctypes.Structure):
+    _fields_ = [("n_features", ctypes.c_int32), ("group_factor", ctypes.c_void_p),
+                ("group_count", ctypes.c_void_p), ("n_groups", ctypes.c_int32),
+                ("thresholds", ctypes.c_void_p), ("stc", ctypes.c_void_p),
+                ("cond_indices", ctypes.c_void_p), ("leaves", ctypes.c_void_p),
+                ("scale", ctypes.c_double), ("bias", ctypes.c_double),
+                ("device", ctypes.c_int32)]
+
+
 _lib = None
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -80,6 +89,8 @@ def lib():
                                  ctypes.POINTER(_vp)]
     L.odf_load_model_ex.restype = ctypes.c_int
     L.odf_load_model_ex.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(_vp)]
+    L.odf_load_model_paper.restype = ctypes.c_int
+    L.odf_load_model_paper.argtypes = [ctypes.POINTER(_PaperDesc), ctypes.POINTER(_vp)]
     L.odf_score_u64.restype = ctypes.c_int
     L.odf_score_u64.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp]
     L.odf_apply_u64.restype = ctypes.c_int
@@ -115,7 +126,7 @@ ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_mode
                "odf_get_info", "odf_bins_layout", "odf_binarize", "odf_apply", "odf_score",
                "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host",
                "odf_latency_workspace_bytes", "odf_score_latency", "odf_load_model_ex",
-               "odf_score_u64", "odf_apply_u64")
+               "odf_score_u64", "odf_apply_u64", "odf_load_model_paper")
 
 
 def _check(status: int):
@@ -161,15 +172,41 @@ class Model:
                   int(n_features), int(device), float(scale), float(bias))
         h = _vp()
         _check(L.odf_load_model_ex(ctypes.byref(d), ctypes.byref(h)))
-        self.leaf_type = "u32" if u32 else "f32"
+        self._init_from_handle(h, device)
+
+    @classmethod
+    def from_paper(cls, n_features, group_factor, group_count, thresholds, stc, cond_indices,
+                   leaves, scale=1.0, bias=0.0, device: int = 0) -> "Model":
+        """Import the paper's model layout: see odf_load_model_paper."""
+        gf = np.ascontiguousarray(group_factor, dtype=np.int32)
+        gc = np.ascontiguousarray(group_count, dtype=np.int32)
+        th = np.ascontiguousarray(thresholds, dtype=np.float32)
+        st = np.zeros(MAX_DEPTH + 1, np.int32)
+        st[:len(stc)] = np.asarray(stc, dtype=np.int32)
+        ci = np.ascontiguousarray(cond_indices, dtype=np.uint32)
+        lv = np.ascontiguousarray(leaves, dtype=np.uint32)
+        d = _PaperDesc(int(n_features), gf.ctypes.data if gf.size else None,
+                       gc.ctypes.data if gc.size else None, gf.size,
+                       th.ctypes.data if th.size else None, st.ctypes.data,
+                       ci.ctypes.data if ci.size else None, lv.ctypes.data if lv.size else None,
+                       float(scale), float(bias), int(device))
+        h = _vp()
+        _check(lib().odf_load_model_paper(ctypes.byref(d), ctypes.byref(h)))
+        self = cls.__new__(cls)
+        self._init_from_handle(h, device)
+        return self
+
+    def _init_from_handle(self, h, device):
+        L = lib()
         self._h = h
         self.device = int(device)
-        self.depth = depth
-        self.n_trees = int(n_trees)
-        self.n_features = int(n_features)
         inf = _Info()
         _check(L.odf_get_info(self._h, ctypes.byref(inf)))
         self.info = {k: getattr(inf, k) for k, _ in _Info._fields_}
+        self.depth = int(inf.depth)
+        self.n_trees = int(inf.n_trees)
+        self.n_features = int(inf.n_features)
+        self.leaf_type = "u32" if inf.leaf_type == 1 else "f32"
         n = _i32()
         ids = ctypes.POINTER(_i32)()
         nb = ctypes.c_size_t()

@@ -225,3 +225,38 @@ def make_case(name: str, n_docs: int | None = None, exact_leaves: bool = False,
 def latency_queries(seed: int, pool_docs: int, batch: int, n_queries: int) -> np.ndarray:
     """Config 5: query q scores docs [o_q, o_q + batch) of the pool."""
     return _rng(seed, _P_QUERY, batch).integers(0, pool_docs - batch + 1, n_queries)
+
+
+@dataclass
+class PaperModel:
+    """The paper's model layout, for the paper-native import (NEXT-2)."""
+    n_features: int
+    group_factor: np.ndarray   # int32 [n_groups]
+    group_count: np.ndarray    # int32 [n_groups]
+    thresholds: np.ndarray     # float32 [K]
+    stc: np.ndarray            # int32 [9], trees per height 0..8
+    cond_indices: np.ndarray   # uint32 [sum h*stc[h]], trees in descending height
+    leaves: np.ndarray         # uint32 [sum 2^h*stc[h]]
+    scale: float = 1.0
+    bias: float = 0.0
+
+
+def paper_model(seed: int, n_features: int, n_binary: int, stc) -> PaperModel:
+    """A synthetic model of the paper's shape: n_binary binary features spread
+    round-robin over the factors (one descriptor group per factor),
+    thresholds U[0,1), condition indices uniform over the binary features, u32
+    answers uniform over the full range, STC[h] trees of height h stored in
+    descending height.  Table 6.1's synthetic model is
+    n_binary=100 with 100 trees of each height."""
+    g = _rng(seed, _P_THR, 99)
+    base, extra = divmod(n_binary, n_features)
+    counts = np.array([base + (1 if f < extra else 0) for f in range(n_features)], np.int32)
+    gf = np.flatnonzero(counts > 0).astype(np.int32)
+    gc = counts[gf]
+    thr = np.concatenate([np.sort(g.random(c, dtype=np.float32)) for c in gc]) if gc.size else \
+        np.zeros(0, np.float32)
+    stc = np.asarray(stc, np.int32)
+    heights = [h for h in range(len(stc) - 1, -1, -1) for _ in range(stc[h])]
+    ci = g.integers(0, max(n_binary, 1), sum(heights)).astype(np.uint32)
+    lv = g.integers(0, 2 ** 32, sum(1 << h for h in heights), dtype=np.uint64).astype(np.uint32)
+    return PaperModel(n_features, gf, gc, thr.astype(np.float32), stc, ci, lv)

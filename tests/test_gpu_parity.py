@@ -346,3 +346,35 @@ def test_integer_leaves_exact(depth, n_docs, n_trees):
         m.score(x)
     torch.cuda.synchronize()
     m.close()
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: paper-native mixed-height model import, exact u64 parity
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("stc,n_binary,n_features", [
+    ([100] * 9, 100, 100),             # Table 6.1 synthetic: 100 trees of each height 0..8
+    ([3, 0, 5, 0, 0, 0, 40, 0, 0], 150, 20),
+    ([0, 0, 0, 0, 0, 0, 64, 0, 0], 64, 64),
+    ([7, 0, 0, 0, 0, 0, 0, 0, 0], 10, 4),   # only constant (height-0) trees
+])
+def test_paper_native_import(stc, n_binary, n_features):
+    import torch
+    from paper_2205_07307_b200 import Model
+    pm = synth.paper_model(11, n_features, n_binary, stc)
+    pm.scale, pm.bias = 2.0 ** -31, 1.5
+    rng = np.random.default_rng(3)
+    D = 1024
+    x = np.zeros((D, (n_features + 3) // 4 * 4), np.float32)
+    x[:, :n_features] = rng.random((D, n_features), dtype=np.float32)
+    for _ in range(500):  # ties with thresholds
+        k = rng.integers(pm.thresholds.size)
+        f = np.repeat(pm.group_factor, pm.group_count)[k]
+        x[rng.integers(D), f] = pm.thresholds[k]
+    m = Model.from_paper(pm.n_features, pm.group_factor, pm.group_count, pm.thresholds, pm.stc,
+                         pm.cond_indices, pm.leaves, pm.scale, pm.bias)
+    sums, sc = m.score_u64(torch.from_numpy(x).cuda())
+    want = oracle.apply_paper(x, pm.group_factor, pm.group_count, pm.thresholds, pm.stc,
+                              pm.cond_indices, pm.leaves)
+    assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
+    assert np.array_equal(sc.cpu().numpy(), oracle.finalize(want, pm.scale, pm.bias))
+    m.close()
