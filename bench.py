@@ -98,6 +98,18 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _traffic(cfg: str):
+    """dram read+write bytes per launch of the fused kernel from the latest committed
+    ncu --set full capture (profiles/rN_traffic.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            return int(json.load(open(path))[cfg]["fused"]["dram_bytes_per_launch"]), path
+        except Exception:
+            continue
+    return None, None
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -144,9 +156,11 @@ def run_reference(args):
     case = _workload(args.config, 0)
     times = []
     base = None
+    # each step is a bounded sample; the whole W+K run stays within ~2 minutes
+    per_step = max(0.25, min(args.ref_seconds, 120.0 / (args.warmup + args.steps)))
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        cb = cpu_baseline(case, target_s=args.ref_seconds)
+        cb = cpu_baseline(case, target_s=per_step)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(cb["value"])
@@ -263,6 +277,7 @@ def run_ours(args):
         value = docs_total / (total_ms / 1000.0)
         alg_bytes = n * (4 * info["n_used_features"] + 4)  # fused = 4*F_used + 4
         achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
+        traffic, traffic_src = (args.traffic, "--traffic") if args.traffic else _traffic(args.config)
         line = {
             "metric": METRIC, "value": value, "unit": "docs/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -276,7 +291,7 @@ def run_ours(args):
                        "parallelism": f"doc-shard x{ws}"},
             "doc_trees_per_s": value * case.n_trees,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": args.traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_kind": peak_kind, "kernel": "odf_main_kernel<FUSED,%d>" % case.depth,
                          "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes},
             "two_stage": {"binarize_ms": tb, "apply_ms": ta,
