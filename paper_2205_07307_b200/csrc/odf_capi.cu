@@ -488,6 +488,16 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
                               static_cast<uint32_t>(used_of[f]) * kTile,
                               colB_of[f] >= 0 ? static_cast<uint32_t>(colB_of[f]) * kTile : kNoCol);
     }
+    // SIMPLE pairs (kind bit 0x10): both factors used and neither has a second column,
+    // so the kernel stores the bin directly as the code
+    for (size_t f = 0; f + 1 < fmeta.size(); f += 2) {
+        const bool ua = f < static_cast<size_t>(n_features) && !borders[f].empty();
+        const bool ub = f + 1 < static_cast<size_t>(n_features) && !borders[f + 1].empty();
+        if (ua && ub && borders[f].size() <= 127 && borders[f + 1].size() <= 127) {
+            fmeta[f].y |= 0x10u;
+            fmeta[f + 1].y |= 0x10u;
+        }
+    }
     // the unused factor of a mixed pair searches its partner's array and stores nothing
     for (size_t f = 0; f + 1 < fmeta.size(); f += 2) {
         const bool ua = f < static_cast<size_t>(n_features) && !borders[f].empty();
@@ -501,8 +511,8 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     for (int32_t c = 0; c < m->n_fchunks; ++c) {
         uint32_t lo = UINT32_MAX, hi = 0;
         for (int32_t f = c * kFSub; f < (c + 1) * kFSub; ++f) {
-            if ((fmeta[f].y & 0xffu) == 0) continue;
-            const uint32_t kf = fmeta[f].y & 0xffu;
+            if ((fmeta[f].y & 0xfu) == 0) continue;
+            const uint32_t kf = fmeta[f].y & 0xfu;
             const uint32_t L = (fmeta[f].y >> 8) & 0xffu;
             const uint32_t len = kf == 1 ? 4u : skew_h((1u << L) - 2u) + 1u;
             lo = std::min(lo, fmeta[f].x);
@@ -510,7 +520,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         }
         if (hi == 0) continue;
         for (int32_t f = c * kFSub; f < (c + 1) * kFSub; ++f)
-            if ((fmeta[f].y & 0xffu) != 0) fmeta[f].x -= lo;
+            if ((fmeta[f].y & 0xfu) != 0) fmeta[f].x -= lo;
         bchunk[c] = make_uint2(lo * 4u, (hi - lo) * 4u);
         m->bord_stride = std::max(m->bord_stride, (hi - lo) * 4u);
     }

@@ -238,45 +238,81 @@ __device__ __forceinline__ void store_bin(const Sink &bins, const uint4 &m, int 
     }
 }
 
+// Store of a SIMPLE pair (both factors used, <= 127 borders): the bin is its own code.
+template <class Sink>
+__device__ __forceinline__ void store_simple(const Sink &bins, const uint4 &m, int doc, uint32_t bin)
+{
+    bins.st(m.z + doc, bin);
+}
+
 // x = {a@doc0, a@doc1, b@doc0, b@doc1}
-template <bool CODES, int L, class Sink>
+template <bool CODES, int L, class Sink, bool SIMPLE>
 __device__ __forceinline__ void bin_pair(const float x[4], const uint4 &ma, const uint4 &mb,
                                          uint32_t bord, const Sink &bins, int d0, int d1)
 {
     const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
     uint32_t pos[4] = {a0, a0, b0, b0};
     search4<L>(x, pos);
-    store_bin<CODES, Sink>(bins, ma, d0, pos_to_bin<L>(pos[0], a0, ma.y >> 16));
-    store_bin<CODES, Sink>(bins, ma, d1, pos_to_bin<L>(pos[1], a0, ma.y >> 16));
-    store_bin<CODES, Sink>(bins, mb, d0, pos_to_bin<L>(pos[2], b0, mb.y >> 16));
-    store_bin<CODES, Sink>(bins, mb, d1, pos_to_bin<L>(pos[3], b0, mb.y >> 16));
+    const uint32_t r0 = pos_to_bin<L>(pos[0], a0, ma.y >> 16), r1 = pos_to_bin<L>(pos[1], a0, ma.y >> 16);
+    const uint32_t r2 = pos_to_bin<L>(pos[2], b0, mb.y >> 16), r3 = pos_to_bin<L>(pos[3], b0, mb.y >> 16);
+    if (SIMPLE) {
+        store_simple(bins, ma, d0, r0);
+        store_simple(bins, ma, d1, r1);
+        store_simple(bins, mb, d0, r2);
+        store_simple(bins, mb, d1, r3);
+    } else {
+        store_bin<CODES, Sink>(bins, ma, d0, r0);
+        store_bin<CODES, Sink>(bins, ma, d1, r1);
+        store_bin<CODES, Sink>(bins, mb, d0, r2);
+        store_bin<CODES, Sink>(bins, mb, d1, r3);
+    }
+}
+
+template <bool CODES, class Sink, bool SIMPLE>
+__device__ __forceinline__ void pair_dispatch_k(const float x[4], const uint4 &ma, const uint4 &mb,
+                                                uint32_t bord, const Sink &bins, int d0, int d1)
+{
+    const uint32_t kind = ma.y & 0xfu;
+    if (kind == BK_LIN4) {
+        const float4 ba = lds_v4f(bord + ma.x * 4u);
+        const float4 bb = lds_v4f(bord + mb.x * 4u);
+        const uint32_t r0 = min(ge4(x[0], ba), ma.y >> 16), r1 = min(ge4(x[1], ba), ma.y >> 16);
+        const uint32_t r2 = min(ge4(x[2], bb), mb.y >> 16), r3 = min(ge4(x[3], bb), mb.y >> 16);
+        if (SIMPLE) {
+            store_simple(bins, ma, d0, r0);
+            store_simple(bins, ma, d1, r1);
+            store_simple(bins, mb, d0, r2);
+            store_simple(bins, mb, d1, r3);
+        } else {
+            store_bin<CODES, Sink>(bins, ma, d0, r0);
+            store_bin<CODES, Sink>(bins, ma, d1, r1);
+            store_bin<CODES, Sink>(bins, mb, d0, r2);
+            store_bin<CODES, Sink>(bins, mb, d1, r3);
+        }
+        return;
+    }
+    switch ((ma.y >> 8) & 0xffu) {
+    case 1: bin_pair<CODES, 1, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    case 2: bin_pair<CODES, 2, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    case 3: bin_pair<CODES, 3, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    case 4: bin_pair<CODES, 4, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    case 5: bin_pair<CODES, 5, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    case 6: bin_pair<CODES, 6, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    case 7: bin_pair<CODES, 7, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    default: bin_pair<CODES, 8, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    }
 }
 
 template <bool CODES, class Sink>
 __device__ __forceinline__ void pair_dispatch(const float x[4], const uint4 &ma, const uint4 &mb,
                                               uint32_t bord, const Sink &bins, int d0, int d1)
 {
-    const uint32_t kind = ma.y & 0xffu;
-    if (kind == BK_SKIP) return;  // warp-uniform
-    if (kind == BK_LIN4) {
-        const float4 ba = lds_v4f(bord + ma.x * 4u);
-        const float4 bb = lds_v4f(bord + mb.x * 4u);
-        store_bin<CODES, Sink>(bins, ma, d0, min(ge4(x[0], ba), ma.y >> 16));
-        store_bin<CODES, Sink>(bins, ma, d1, min(ge4(x[1], ba), ma.y >> 16));
-        store_bin<CODES, Sink>(bins, mb, d0, min(ge4(x[2], bb), mb.y >> 16));
-        store_bin<CODES, Sink>(bins, mb, d1, min(ge4(x[3], bb), mb.y >> 16));
-        return;
-    }
-    switch ((ma.y >> 8) & 0xffu) {
-    case 1: bin_pair<CODES, 1, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    case 2: bin_pair<CODES, 2, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    case 3: bin_pair<CODES, 3, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    case 4: bin_pair<CODES, 4, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    case 5: bin_pair<CODES, 5, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    case 6: bin_pair<CODES, 6, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    case 7: bin_pair<CODES, 7, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    default: bin_pair<CODES, 8, Sink>(x, ma, mb, bord, bins, d0, d1); break;
-    }
+    if ((ma.y & 0xfu) == BK_SKIP) return;  // warp-uniform
+    // simple pair: both factors used, no second code column (set by the model compiler)
+    if (ma.y & 0x10u)
+        pair_dispatch_k<CODES, Sink, true>(x, ma, mb, bord, bins, d0, d1);
+    else
+        pair_dispatch_k<CODES, Sink, false>(x, ma, mb, bord, bins, d0, d1);
 }
 
 // tile: the 16 KB factor box; meta: its 32 fmeta entries (512 B); bord: its
@@ -291,7 +327,7 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
     const int d0 = ((warp & 1) << 6) | lane, d1 = d0 + 32;
     const uint4 m0 = lds_v4u(meta + 64u * q), m1 = lds_v4u(meta + 64u * q + 16u);
     const uint4 m2 = lds_v4u(meta + 64u * q + 32u), m3 = lds_v4u(meta + 64u * q + 48u);
-    if (((m0.y | m2.y) & 0xffu) == BK_SKIP) return;  // warp-uniform: no used factor in the quad
+    if (((m0.y | m2.y) & 0xfu) == BK_SKIP) return;  // warp-uniform: no used factor in the quad
     const float4 v0 = lds_v4f(tile + d0 * 128 + ((q ^ (d0 & 7)) << 4));
     const float4 v1 = lds_v4f(tile + d1 * 128 + ((q ^ (d1 & 7)) << 4));
     {
