@@ -177,6 +177,16 @@ ODF_API odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t 
 ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
                      float *d_scores, void *stream);
 
+/* Feature-major input (NEXT-4; the paper's pre-transposed variant, §5.5):
+ * d_factors_fm [n_features x ld_fm] fp32 row-major, i.e. factor f of document i at
+ * d_factors_fm[f*ld_fm + i]; ld_fm >= n_docs, ld_fm % 4 == 0, 16-byte aligned.
+ * Same bins / scores as odf_binarize / odf_score on the transposed matrix
+ * (bit-identical).  The TMA box is (128 docs x 32 factors), unswizzled.       */
+ODF_API odf_status odf_binarize_fm(const odf_model *m, const float *d_factors_fm, int64_t n_docs,
+                                   int64_t ld_fm, uint8_t *d_bins, void *stream);
+ODF_API odf_status odf_score_fm(const odf_model *m, const float *d_factors_fm, int64_t n_docs,
+                                int64_t ld_fm, float *d_scores, void *stream);
+
 /* Integer-leaf models (ODF_LEAF_U32): fused (from factors) and stage-2 (from
  * bins) scoring into d_sums [n_docs] uint64 (R, exact) and/or d_scores [n_docs]
  * double ((R - 2^31) * S + B, each operation rounded to nearest, no FMA); either

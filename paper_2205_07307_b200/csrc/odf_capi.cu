@@ -157,7 +157,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
 }
 
 odf_status encode_tmap(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld,
-                       CUtensorMap *tm)
+                       CUtensorMap *tm, bool fm = false)
 {
     std::call_once(g_encode_once, [] {
         void *fn = nullptr;
@@ -168,14 +168,18 @@ odf_status encode_tmap(const odf_model *m, const float *d_x, int64_t n_docs, int
             g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     });
     if (!g_encode) return fail(ODF_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(m->n_features), static_cast<cuuint64_t>(n_docs)};
+    // doc-major: dims (factors, docs), box (32, 128), 128B swizzle;
+    // feature-major (NEXT-4): dims (docs, factors), box (128, 32), 512-byte rows, no swizzle
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(fm ? n_docs : m->n_features),
+                          static_cast<cuuint64_t>(fm ? m->n_features : n_docs)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kFSub), static_cast<cuuint32_t>(kTile)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(fm ? kTile : kFSub),
+                         static_cast<cuuint32_t>(fm ? kFSub : kTile)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(d_x), dims,
                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          fm ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(ODF_E_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
     return ODF_OK;
 }
@@ -213,6 +217,18 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.off_bord = pl.off_bord;
     p.bord_stride = m->bord_stride;
     return p;
+}
+
+odf_status check_factors_fm(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld)
+{
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs >= (int64_t(1) << 31) - kTile)
+        return fail(ODF_E_INVALID_ARG, "n_docs >= 2^31 - 128 (TMA coordinate range)");
+    if (ld < n_docs) return fail(ODF_E_INVALID_ARG, "ld_fm (%lld) < n_docs (%lld)", (long long)ld, (long long)n_docs);
+    if (ld % 4 != 0) return fail(ODF_E_INVALID_ARG, "ld_fm %% 4 != 0 (rows must be 16-byte aligned for TMA)");
+    if (n_docs > 0 && !d_x) return fail(ODF_E_INVALID_ARG, "d_factors is NULL");
+    if (reinterpret_cast<uintptr_t>(d_x) % 16 != 0) return fail(ODF_E_INVALID_ARG, "d_factors not 16-byte aligned");
+    return ODF_OK;
 }
 
 odf_status check_factors(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld)
@@ -650,7 +666,7 @@ odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
 
 static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64_t n_docs, int64_t ld,
                            const uint8_t *bins_in, uint8_t *bins_out, float *scores, cudaStream_t s,
-                           uint64_t *sums = nullptr, double *dscores = nullptr)
+                           uint64_t *sums = nullptr, double *dscores = nullptr, bool fm = false)
 {
     const Plan &pl = mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
     KParams p = base_params(m, pl);
@@ -663,8 +679,9 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     p.dscores = dscores;
     CUtensorMap tm;
     const CUtensorMap *tmp = nullptr;
+    p.fm = fm ? 1 : 0;
     if (mode != MODE_APPLY && p.n_fchunks > 0) {
-        odf_status st = encode_tmap(m, d_x, n_docs, ld, &tm);
+        odf_status st = encode_tmap(m, d_x, n_docs, ld, &tm, fm);
         if (st != ODF_OK) return st;
         tmp = &tm;
     }
@@ -715,6 +732,31 @@ odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs,
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
     return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, d_scores,
                     static_cast<cudaStream_t>(stream));
+}
+
+odf_status odf_binarize_fm(const odf_model *m, const float *d_factors_fm, int64_t n_docs,
+                           int64_t ld_fm, uint8_t *d_bins, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    odf_status st = check_factors_fm(m, d_factors_fm, n_docs, ld_fm);
+    if (st != ODF_OK) return st;
+    if (n_docs == 0 || m->n_used == 0) return ok();
+    if (!d_bins) return fail(ODF_E_INVALID_ARG, "d_bins is NULL");
+    return run_main(m, MODE_BINARIZE, d_factors_fm, n_docs, ld_fm, nullptr, d_bins, nullptr,
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr, true);
+}
+
+odf_status odf_score_fm(const odf_model *m, const float *d_factors_fm, int64_t n_docs, int64_t ld_fm,
+                        float *d_scores, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "integer-leaf model: use odf_score_u64");
+    odf_status st = check_factors_fm(m, d_factors_fm, n_docs, ld_fm);
+    if (st != ODF_OK) return st;
+    if (n_docs == 0) return ok();
+    if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    return run_main(m, MODE_FUSED, d_factors_fm, n_docs, ld_fm, nullptr, nullptr, d_scores,
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr, true);
 }
 
 odf_status odf_score_u64(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,

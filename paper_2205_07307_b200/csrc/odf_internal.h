@@ -31,6 +31,7 @@ struct KParams {
     const uint2 *bchunk;    // [n_fchunks] {byte offset into borders, bytes} of each sub-tile's
                             // border arrays (fmeta.x is relative to that offset)
     int32_t n_fchunks;      // ceil(n_features / 32), 0 if no used factor
+    int32_t fm;             // 1: factors are feature-major [n_features][ld] (NEXT-4)
     // ---- apply (stage 2) ----
     const uint8_t *chunks;  // [n_tchunks][chunk_bytes]: descriptors then reversed leaf tables
     int32_t n_tchunks;

@@ -321,15 +321,24 @@ __device__ __forceinline__ void pair_dispatch(const float x[4], const uint4 &ma,
 // + 32: 4 independent search chains per lane per pair.
 template <bool CODES, class Sink>
 __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
-                                             const Sink &bins, int warp, int lane)
+                                             const Sink &bins, int warp, int lane, bool fm)
 {
     const int q = warp >> 1;
     const int d0 = ((warp & 1) << 6) | lane, d1 = d0 + 32;
     const uint4 m0 = lds_v4u(meta + 64u * q), m1 = lds_v4u(meta + 64u * q + 16u);
     const uint4 m2 = lds_v4u(meta + 64u * q + 32u), m3 = lds_v4u(meta + 64u * q + 48u);
     if (((m0.y | m2.y) & 0xfu) == BK_SKIP) return;  // warp-uniform: no used factor in the quad
-    const float4 v0 = lds_v4f(tile + d0 * 128 + ((q ^ (d0 & 7)) << 4));
-    const float4 v1 = lds_v4f(tile + d1 * 128 + ((q ^ (d1 & 7)) << 4));
+    float4 v0, v1;
+    if (fm) {  // feature-major box [32 factors][128 docs]: 512-byte rows, lanes = docs
+        const uint32_t r = tile + q * 4 * 512;
+        v0 = make_float4(lds_f32(r + d0 * 4), lds_f32(r + 512 + d0 * 4), lds_f32(r + 1024 + d0 * 4),
+                         lds_f32(r + 1536 + d0 * 4));
+        v1 = make_float4(lds_f32(r + d1 * 4), lds_f32(r + 512 + d1 * 4), lds_f32(r + 1024 + d1 * 4),
+                         lds_f32(r + 1536 + d1 * 4));
+    } else {   // doc-major box [128 docs][32 factors], 128B-swizzled
+        v0 = lds_v4f(tile + d0 * 128 + ((q ^ (d0 & 7)) << 4));
+        v1 = lds_v4f(tile + d1 * 128 + ((q ^ (d1 & 7)) << 4));
+    }
     {
         const float x[4] = {v0.x, v1.x, v0.y, v1.y};
         pair_dispatch<CODES, Sink>(x, m0, m1, bord, bins, d0, d1);
@@ -568,8 +577,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_expect_tx(full, tx);
                     for (int s = 0; s < nsub; ++s) {
                         const int c = c0 + s;
-                        tma_load_2d(sb + s * kFSubBytes, &tmap, c * kFSub,
-                                    static_cast<int>(tile * kTile), full);
+                        if (p.fm)  // feature-major input (NEXT-4): box (128 docs, 32 factors)
+                            tma_load_2d(sb + s * kFSubBytes, &tmap, static_cast<int>(tile * kTile),
+                                        c * kFSub, full);
+                        else
+                            tma_load_2d(sb + s * kFSubBytes, &tmap, c * kFSub,
+                                        static_cast<int>(tile * kTile), full);
                         bulk_g2s(sb + p.off_meta + s * kMetaBytes, p.fmeta + c * kFSub, kMetaBytes,
                                  full);
                         const uint2 bc = sld<uint2>(bct + 8u * c);
@@ -611,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int s = 0; s < nsub; ++s)
                     binarize_sub<MODE == MODE_FUSED, SmemSink>(
                         sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
-                        sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp, lane);
+                        sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp, lane, p.fm != 0);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty);
                 if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -756,7 +769,10 @@ __global__ void __launch_bounds__(kConsumerThreads)
         fence_barrier_init();
         const uint2 bc = p.bchunk[c];
         mbar_expect_tx(bar, kFSubBytes + kMetaBytes + bc.y);
-        tma_load_2d(t_off, &tmap, c * kFSub, static_cast<int>(tile * kTile), bar);
+        if (p.fm)
+            tma_load_2d(t_off, &tmap, static_cast<int>(tile * kTile), c * kFSub, bar);
+        else
+            tma_load_2d(t_off, &tmap, c * kFSub, static_cast<int>(tile * kTile), bar);
         bulk_g2s(m_off, p.fmeta + c * kFSub, kMetaBytes, bar);
         if (bc.y) bulk_g2s(b_off, reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, bar);
         if (c == 0) p.lat_counter[tile] = 0u;  // ticket for kernel (2), stream-ordered
@@ -765,7 +781,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     mbar_wait(bar, 0);
     binarize_sub<true, GmemSink>(t_off, m_off, b_off,
                                  GmemSink{p.lat_codes + tile * static_cast<int64_t>(p.n_cols) * kTile},
-                                 warp, lane);
+                                 warp, lane, p.fm != 0);
 }
 
 template <int DEPTH>

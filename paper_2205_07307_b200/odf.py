@@ -91,6 +91,10 @@ def lib():
     L.odf_load_model_ex.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(_vp)]
     L.odf_load_model_paper.restype = ctypes.c_int
     L.odf_load_model_paper.argtypes = [ctypes.POINTER(_PaperDesc), ctypes.POINTER(_vp)]
+    L.odf_binarize_fm.restype = ctypes.c_int
+    L.odf_binarize_fm.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+    L.odf_score_fm.restype = ctypes.c_int
+    L.odf_score_fm.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
     L.odf_score_u64.restype = ctypes.c_int
     L.odf_score_u64.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp]
     L.odf_apply_u64.restype = ctypes.c_int
@@ -126,7 +130,8 @@ ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_mode
                "odf_get_info", "odf_bins_layout", "odf_binarize", "odf_apply", "odf_score",
                "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host",
                "odf_latency_workspace_bytes", "odf_score_latency", "odf_load_model_ex",
-               "odf_score_u64", "odf_apply_u64", "odf_load_model_paper")
+               "odf_score_u64", "odf_apply_u64", "odf_load_model_paper", "odf_binarize_fm",
+               "odf_score_fm")
 
 
 def _check(status: int):
@@ -299,6 +304,30 @@ class Model:
         _check(lib().odf_apply_u64(self._h, _ptr(bins), int(n_docs), _ptr(sums), _ptr(sc),
                                    _stream(stream, self._dev())))
         return sums, sc
+
+    def _check_xt(self, xt: torch.Tensor, n_docs: int):
+        if not (xt.is_cuda and xt.dtype == torch.float32 and xt.dim() == 2 and xt.stride(1) == 1
+                and xt.shape[0] >= self.n_features and xt.shape[1] >= n_docs):
+            raise OdfError(1, "feature-major factors must be a CUDA float32 [>= n_features, "
+                              ">= n_docs] tensor with unit column stride")
+        return xt.stride(0)
+
+    def binarize_fm(self, xt: torch.Tensor, n_docs: int, out=None, stream=None):
+        """Feature-major input (NEXT-4): xt[f, i] = factor f of document i."""
+        ld = self._check_xt(xt, n_docs)
+        if out is None:
+            out = torch.empty(self.bins_bytes(n_docs), dtype=torch.uint8, device=self._dev())
+        _check(lib().odf_binarize_fm(self._h, _ptr(xt), int(n_docs), ld, _ptr(out),
+                                     _stream(stream, self._dev())))
+        return out
+
+    def score_fm(self, xt: torch.Tensor, n_docs: int, out=None, stream=None):
+        ld = self._check_xt(xt, n_docs)
+        if out is None:
+            out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
+        _check(lib().odf_score_fm(self._h, _ptr(xt), int(n_docs), ld, _ptr(out),
+                                  _stream(stream, self._dev())))
+        return out
 
     def score_host(self, x, out=None, chunk_docs: int = 65536, stream=None):
         """End-to-end from host memory (numpy array or CPU tensor, ideally pinned)."""

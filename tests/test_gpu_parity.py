@@ -378,3 +378,30 @@ def test_paper_native_import(stc, n_binary, n_features):
     assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
     assert np.array_equal(sc.cpu().numpy(), oracle.finalize(want, pm.scale, pm.bias))
     m.close()
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: feature-major (pre-transposed, §5.5) input, bit-identical to doc-major
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n_docs,name", [(1, "c1"), (129, "c1"), (1024, "c1"), (3000, "c2"),
+                                         (777, "c4")])
+def test_feature_major_input(n_docs, name):
+    import torch
+    case = synth.make_case(name, n_docs=n_docs, n_trees=None if name == "c1" else 300)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    ldt = (n_docs + 3) // 4 * 4 + 4
+    xt_h = np.full((case.n_features, ldt), np.nan, np.float32)
+    xt_h[:, :n_docs] = case.x[:, :case.n_features].T
+    xt = to_dev(xt_h)
+    b_dm = m.binarize(x)
+    b_fm = m.binarize_fm(xt, n_docs)
+    assert np.array_equal(m.canonical_bins(b_fm, n_docs).cpu().numpy(),
+                          m.canonical_bins(b_dm, n_docs).cpu().numpy())
+    s_dm = m.score(x).cpu().numpy()
+    s_fm = m.score_fm(xt, n_docs).cpu().numpy()
+    assert np.array_equal(s_dm.view(np.uint32), s_fm.view(np.uint32))
+    want_bins, _, _ = oracle_bins_used(case)
+    assert np.array_equal(m.canonical_bins(b_fm, n_docs).cpu().numpy(), want_bins)
+    torch.cuda.synchronize()
+    m.close()
