@@ -405,3 +405,29 @@ def test_feature_major_input(n_docs, name):
     assert np.array_equal(m.canonical_bins(b_fm, n_docs).cpu().numpy(), want_bins)
     torch.cuda.synchronize()
     m.close()
+
+
+# ---------------------------------------------------------------------------
+# tree sharding on one GPU: per-shard partials summed == whole forest (tolerance / exact)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("world,exact", [(2, False), (3, True), (8, False)])
+def test_tree_shards_sum_to_forest(world, exact):
+    import torch
+    from paper_2205_07307_b200 import Model
+    from paper_2205_07307_b200.parallel import tree_shard
+    case = synth.make_case("c4", n_docs=2000, n_trees=203, exact_leaves=exact)
+    x = to_dev(case.x)
+    total = torch.zeros(case.n_docs, dtype=torch.float32, device="cuda")
+    for r in range(world):
+        fi, th, lv, _ = tree_shard(case.feature_index, case.thresholds, case.leaf_values,
+                                   case.depth, world, r)
+        m = Model(fi, th, lv, case.depth, case.n_features)
+        total += m.score(x)
+        m.close()
+    got = total.cpu().numpy()
+    s64, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values,
+                            case.depth)
+    if exact:
+        assert np.array_equal(got, s32)
+    else:
+        assert np.abs(got - s64).max() <= tolerance(case.leaf_values, case.depth)
