@@ -114,7 +114,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
     const uint32_t bins = align_up(static_cast<uint64_t>(cols) * kTile, 1024);
     const uint32_t red_bytes = m.leaf_u32 ? 2 * kRedBytes : kRedBytes;
     const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes);
-    const uint32_t bars = align_up(16u * 8 + 16 + 8u * m.n_fchunks, 128);  // + bchunk copy
+    const uint32_t bars = align_up(160 + 8u * m.n_fchunks, 128);  // barriers, scratch, bchunk copy
     // a factor sub-tile travels as [16 KB box][512 B fmeta][its border arrays]
     const uint32_t unit = kFSubBytes + kMetaBytes + m.bord_stride;
     uint32_t slot;
@@ -542,14 +542,21 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     }
 
     // ---- tree chunks: descriptors + reversed leaf tables ----
-    const int dstride = ((depth + 1) & ~1) * 8;
-    m->table_stride = depth <= 6 ? 256u : (4u << depth);
-    const uint32_t per_tree = static_cast<uint32_t>(dstride) + m->table_stride;
-    m->tc = 16 * std::max<uint32_t>(1u, 20480u / (16u * per_tree));
+    const int dstride = desc_stride(depth);
+    m->table_stride = static_cast<uint32_t>(table_stride(depth));
+    m->tc = trees_per_chunk(depth);
     m->desc_bytes = align_up(static_cast<uint64_t>(m->tc) * dstride, 256);
     m->chunk_bytes = m->desc_bytes + static_cast<uint32_t>(m->tc) * m->table_stride;
     m->n_tchunks = static_cast<int32_t>((n_trees + m->tc - 1) / m->tc);
     std::vector<uint8_t> chunks(static_cast<size_t>(m->n_tchunks) * m->chunk_bytes, 0);
+    // padding trees of the last chunk: -0.0 answers (x + -0.0 == x bit for bit) / 0
+    if (!u32 && n_trees % m->tc != 0) {
+        uint8_t *ch = chunks.data() + static_cast<size_t>(m->n_tchunks - 1) * m->chunk_bytes;
+        for (int64_t i = n_trees % m->tc; i < m->tc; ++i) {
+            float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
+            for (uint32_t F = 0; F < (1u << depth); ++F) tab[F] = -0.0f;
+        }
+    }
     const uint32_t nleaf = 1u << depth;
     for (int64_t t = 0; t < n_trees; ++t) {
         uint8_t *ch = chunks.data() + static_cast<size_t>(t / m->tc) * m->chunk_bytes;

@@ -17,6 +17,21 @@ constexpr uint32_t kMetaBytes = kFSub * 16;         // fmeta of one sub-tile
 constexpr uint32_t kRedBytes = kConsumerWarps * kTile * 4;
 constexpr uint32_t kNoCol = 0xFFFFFFFFu;
 
+// Tree-chunk geometry, shared by the model compiler and the kernels: per tree the
+// level descriptors (8 B each, padded to an even count) and the reversed leaf table
+// (256 B for depth <= 6 so the PRMT address trick applies, else 4 B * 2^depth);
+// trees per chunk = a multiple of 16 (one tree per consumer warp per round) sized
+// for ~20 KB chunks.  The last chunk is padded with zero-answer trees (-0.0 / 0),
+// so the apply loop has a fixed trip count.
+__host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 1) & ~1) * 8; }
+__host__ __device__ constexpr int table_stride(int depth) { return depth <= 6 ? 256 : (4 << depth); }
+__host__ __device__ constexpr int trees_per_chunk(int depth)
+{
+    return 16 * ((20480 / (16 * (desc_stride(depth) + table_stride(depth)))) > 1
+                     ? (20480 / (16 * (desc_stride(depth) + table_stride(depth))))
+                     : 1);
+}
+
 enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 
 // Per-launch parameters (passed by value; all pointers are device pointers).

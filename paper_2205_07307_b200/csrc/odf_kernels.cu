@@ -433,7 +433,6 @@ __device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint3
     }
 }
 
-__host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 1) & ~1) * 8; }
 
 // Per-lane accumulators of the 4 documents: fp32 leaves summed in fp32 (the
 // north_star's path) or, for MatrixNet integer models, u32 leaves summed in u64
@@ -444,6 +443,19 @@ template <>
 struct Acc<false> {
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     __device__ __forceinline__ void add(int n, uint32_t addr) { v[n] += lds_f32(addr); }
+    // Force the accumulators (hence every gather of the chunk) to be complete before
+    // what follows, i.e. before the mbarrier arrive that hands the slot back to the
+    // producer (ptxas may otherwise sink the FADDs, leaving gathers in flight).
+    __device__ __forceinline__ void pin(uint32_t scratch) const
+    {
+        // a store predicated on all four accumulators (never taken in practice): the
+        // store cannot issue before the FADDs, hence before the gathers returned,
+        // and it is ordered before the (memory) arrive
+        const uint32_t x = __float_as_uint(v[0]) ^ __float_as_uint(v[1]) ^ __float_as_uint(v[2]) ^
+                           __float_as_uint(v[3]);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0x7fc00001;\n\t@p st.shared.u32 [%1], %0;\n\t}"
+                     ::"r"(x), "r"(sabs(scratch)) : "memory");
+    }
     static constexpr uint32_t kRed = kRedBytes;
     __device__ __forceinline__ void to_red(uint32_t red, int warp, int lane) const
     {
@@ -454,6 +466,12 @@ template <>
 struct Acc<true> {
     unsigned long long v[4] = {0ull, 0ull, 0ull, 0ull};
     __device__ __forceinline__ void add(int n, uint32_t addr) { v[n] += lds_u32(addr); }
+    __device__ __forceinline__ void pin(uint32_t scratch) const
+    {
+        const uint32_t x = static_cast<uint32_t>(v[0] ^ v[1] ^ v[2] ^ v[3]);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0x7fc00001;\n\t@p st.shared.u32 [%1], %0;\n\t}"
+                     ::"r"(x), "r"(sabs(scratch)) : "memory");
+    }
     static constexpr uint32_t kRed = 2 * kRedBytes;
     __device__ __forceinline__ void to_red(uint32_t red, int warp, int lane) const
     {
@@ -464,14 +482,15 @@ struct Acc<true> {
 };
 
 template <int DEPTH, bool U32>
-__device__ __forceinline__ void apply_chunk(uint32_t chunk, int n_in, uint32_t desc_bytes,
-                                            uint32_t stride, uint32_t lane_bins, int warp,
-                                            Acc<U32> &acc)
+__device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
+                                            int warp, Acc<U32> &acc)
 {
-#pragma unroll 2
-    for (int i = warp; i < n_in; i += kConsumerWarps) {
+    constexpr int TC = trees_per_chunk(DEPTH);  // chunks are padded to TC trees
+#pragma unroll
+    for (int k = 0; k < TC / kConsumerWarps; ++k) {
+        const int i = warp + k * kConsumerWarps;
         const uint32_t d = chunk + i * desc_stride(DEPTH);
-        const uint32_t tb = chunk + desc_bytes + i * stride;
+        const uint32_t tb = chunk + desc_bytes + i * table_stride(DEPTH);
         uint32_t a[4];
         leaf_addrs<DEPTH>(d, lane_bins, tb, a);
 #pragma unroll
@@ -532,8 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t red = base + p.off_red;
     const uint32_t bars = base + p.off_bars;
     const int S = p.stages;
-    const uint32_t bins_full = bars + 16u * S, bins_empty = bins_full + 8u;
-    const uint32_t bct = bins_empty + 8u;  // [n_fchunks] uint2 copy of p.bchunk
+    // bars: [0,128) full/empty of up to 8 stages, [128,144) bins_full/empty,
+    // [144,160) scratch word for Acc::pin, [160,...) copy of p.bchunk
+    const uint32_t bins_full = bars + 128u, bins_empty = bins_full + 8u;
+    const uint32_t pin_scratch = bars + 144u;
+    const uint32_t bct = bars + 160u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_fjobs = HAS_A ? (p.n_fchunks + p.fsub_per_job - 1) / p.fsub_per_job : 0;
     const int n_bjobs = HAS_B ? p.n_tchunks : 0;
@@ -648,10 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
             mbar_wait(full, ph);
-            const int64_t rem = p.n_trees - static_cast<int64_t>(c) * p.tc;
-            const int n_in = rem < p.tc ? static_cast<int>(rem) : p.tc;
-            apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, n_in, p.desc_bytes,
-                                    p.table_stride, lane_bins, warp, acc);
+            apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, p.desc_bytes, lane_bins, warp, acc);
+            acc.pin(pin_scratch);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty);
             if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -810,9 +830,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         for (uint32_t k = tid; k < p.chunk_bytes / 16; k += kConsumerThreads)
             sts_v4u(chunk + 16 * k, __ldg(src + k));
         __syncthreads();
-        const int64_t rem = p.n_trees - static_cast<int64_t>(c) * p.tc;
-        apply_chunk<DEPTH, false>(chunk, rem < p.tc ? static_cast<int>(rem) : p.tc, p.desc_bytes,
-                                  p.table_stride, lane_bins, warp, acc);
+        apply_chunk<DEPTH, false>(chunk, p.desc_bytes, lane_bins, warp, acc);
     }
     acc.to_red(red, warp, lane);
     __syncthreads();

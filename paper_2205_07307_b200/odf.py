@@ -74,8 +74,8 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if _build._stale():
+    path = os.environ.get("ODF_LIB_OVERRIDE") or _build.LIB  # A/B testing of builds only
+    if path == _build.LIB and _build._stale():
         try:
             _build.build()
         except Exception as e:  # no silent fallback: the CUDA path is the product

@@ -431,3 +431,21 @@ def test_tree_shards_sum_to_forest(world, exact):
         assert np.array_equal(got, s32)
     else:
         assert np.abs(got - s64).max() <= tolerance(case.leaf_values, case.depth)
+
+
+# ---------------------------------------------------------------------------
+# determinism across many tiles and CTAs (WAR hazards on the TMA ring would show here)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n_docs,n_trees", [("c4", 300_000, 1000), ("c2", 300_000, 2000)])
+def test_deterministic_over_many_tiles(name, n_docs, n_trees):
+    import torch
+    case = synth.make_case(name, n_docs=n_docs, n_trees=n_trees)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    ref = m.score(x)
+    bins = m.binarize(x)
+    for _ in range(3):
+        assert torch.equal(m.score(x).view(torch.int32), ref.view(torch.int32))
+        assert torch.equal(m.apply(bins, n_docs).view(torch.int32), ref.view(torch.int32))
+    torch.cuda.synchronize()
+    m.close()
