@@ -187,6 +187,24 @@ ODF_API odf_status odf_binarize_fm(const odf_model *m, const float *d_factors_fm
 ODF_API odf_status odf_score_fm(const odf_model *m, const float *d_factors_fm, int64_t n_docs,
                                 int64_t ld_fm, float *d_scores, void *stream);
 
+/* NEXT-3: bit-packed ordered condition words (the paper's ordered format,
+ * §5.4: "на смещении i стоит бит, соответствующий документу номер i+1").
+ * Binary feature kb = (used factor u, border j) in ascending (u, j); its bit for
+ * document i is the node condition x_i < border_j.  Words: uint32
+ * [ceil(n_docs/32)][n_binary], bit i of word (g, kb) = document 32g + i (0 for
+ * padding documents >= n_docs).
+ * odf_bits_from_bins builds them from blocked bins (one __ballot_sync per binary
+ * feature per 32 documents); odf_apply_bits assembles each leaf index from the
+ * words (§6.4) and returns the same scores as odf_score (same
+ * summation order).  odf_apply_bits: fp32-leaf models whose binary features fit
+ * shared memory (n_binary * 4 B), else ODF_E_UNSUPPORTED.                      */
+ODF_API odf_status odf_bits_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
+                                   int64_t *n_binary_features);
+ODF_API odf_status odf_bits_from_bins(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                                      uint32_t *d_words, void *stream);
+ODF_API odf_status odf_apply_bits(const odf_model *m, const uint32_t *d_words, int64_t n_docs,
+                                  float *d_scores, void *stream);
+
 /* Integer-leaf models (ODF_LEAF_U32): fused (from factors) and stage-2 (from
  * bins) scoring into d_sums [n_docs] uint64 (R, exact) and/or d_scores [n_docs]
  * double ((R - 2^31) * S + B, each operation rounded to nearest, no FMA); either

@@ -82,6 +82,9 @@ def lib():
         L.oracle_apply_paper.restype = None
         L.oracle_apply_paper.argtypes = [_f32p, _i64, _i64, _i32p, _i32p, _i32, _f32p, _i64,
                                          _i32p, _u32p, _u32p, _u64p]
+        L.oracle_condition_words.restype = None
+        L.oracle_condition_words.argtypes = [_f32p, _i64, _i64, _i32, _f32p, _i32p, _i64p, _u32p,
+                                             _i64]
         L.oracle_default_threads.restype = ctypes.c_int
         L.oracle_default_threads.argtypes = []
         _lib = L
@@ -194,6 +197,18 @@ def border_index(feature_index, thresholds, flat, counts, offsets):
     lib().oracle_border_index(fi, _c(thresholds, np.float32), fi.size, fl,
                               _c(counts, np.int32), _c(offsets, np.int64), out)
     return out
+
+
+def condition_words(x, n_features, flat, counts, offsets):
+    """NEXT-3: ordered bit format, words[g, kb] with bit i = condition of doc 32g+i."""
+    x = _x2d(x)
+    n_bin = int(np.asarray(counts).sum())
+    g = (x.shape[0] + 31) // 32
+    out = np.zeros((g, max(n_bin, 1)), np.uint32)
+    fl = _c(flat if flat.size else np.zeros(1, np.float32), np.float32)
+    lib().oracle_condition_words(x, x.shape[0], x.shape[1], int(n_features), fl,
+                                 _c(counts, np.int32), _c(offsets, np.int64), out, max(n_bin, 1))
+    return out[:, :n_bin]
 
 
 def score_u64(x, feature_index, thresholds, leaf_values_u32, depth, n_trees=None, n_threads=0):

@@ -371,3 +371,22 @@ void oracle_apply_paper(const float *x, int64_t n_docs, int64_t ld,
     }
     free(bits);
 }
+
+/* ---- NEXT-3: ordered bit format (§5.4) ------------------------
+ * One binary feature per (used factor f ascending, border j ascending); word g of
+ * binary feature kb holds, at bit i, the condition x[32g + i][f] < borders_f[j]
+ * ("на смещении i стоит бит, соответствующий документу номер i + 1").
+ * Output: words[g * n_binary + kb], g < ceil(n_docs / 32).                   */
+void oracle_condition_words(const float *x, int64_t n_docs, int64_t ld, int32_t n_features,
+                            const float *borders, const int32_t *counts, const int64_t *offsets,
+                            uint32_t *words, int64_t n_binary)
+{
+    int64_t n_groups = (n_docs + 31) / 32;
+    memset(words, 0, sizeof(uint32_t) * (size_t)(n_groups * n_binary));
+    int64_t kb = 0;
+    for (int32_t f = 0; f < n_features; ++f)
+        for (int32_t j = 0; j < counts[f]; ++j, ++kb)
+            for (int64_t i = 0; i < n_docs; ++i)
+                if (oracle_condition(x + i * ld, f, borders[offsets[f] + j]))
+                    words[(i / 32) * n_binary + kb] |= 1u << (i % 32);
+}

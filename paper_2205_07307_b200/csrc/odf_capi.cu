@@ -91,6 +91,8 @@ struct odf_model {
     uint8_t *d_chunks = nullptr;
     uint2 *d_splits = nullptr;
     uint2 *d_bchunk = nullptr;
+    uint32_t *d_bf_base = nullptr, *d_bits_desc = nullptr;  // NEXT-3 (fp32 models)
+    float *d_leaves = nullptr;
     bool leaf_u32 = false;
     double scale = 1.0, bias = 0.0;
     Plan fused, binz, apply;
@@ -271,6 +273,9 @@ void odf_free_model(odf_model *m)
     cudaFree(m->d_chunks);
     cudaFree(m->d_splits);
     cudaFree(m->d_bchunk);
+    cudaFree(m->d_bf_base);
+    cudaFree(m->d_bits_desc);
+    cudaFree(m->d_leaves);
     for (int i = 0; i < 2; ++i) {
         cudaFree(m->d_stage[i]);
         cudaFree(m->d_sstage[i]);
@@ -588,6 +593,23 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         }
     }
 
+    // ---- NEXT-3: binary features (used factor u, border j) and per-level word offsets ----
+    std::vector<uint32_t> bf_base(m->n_used + 1, 0);
+    for (int32_t u = 0; u < m->n_used; ++u)
+        bf_base[u + 1] = bf_base[u] + static_cast<uint32_t>(borders[m->used_ids[u]].size());
+    std::vector<uint32_t> bits_desc;
+    if (!u32) {
+        bits_desc.resize(static_cast<size_t>(n_nodes));
+        for (int64_t k = 0; k < n_nodes; ++k) {
+            const int32_t f = feature_index[k];
+            const auto &b = borders[f];
+            const uint32_t j = static_cast<uint32_t>(
+                std::lower_bound(b.begin(), b.end(), thresholds[k], [](float a, float c) { return a < c; }) -
+                b.begin());
+            bits_desc[k] = (bf_base[used_of[f]] + j) * 4u;
+        }
+    }
+
     // ---- device ----
     int prev = 0;
     cudaGetDevice(&prev);
@@ -610,7 +632,10 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         (e = up(reinterpret_cast<void **>(&m->d_borders), bflat.data(), bflat.size() * 4)) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_chunks), chunks.data(), chunks.size())) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_splits), splits.data(), splits.size() * sizeof(uint2))) != cudaSuccess ||
-        (e = up(reinterpret_cast<void **>(&m->d_bchunk), bchunk.data(), bchunk.size() * sizeof(uint2))) != cudaSuccess) {
+        (e = up(reinterpret_cast<void **>(&m->d_bchunk), bchunk.data(), bchunk.size() * sizeof(uint2))) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_bf_base), bf_base.data(), bf_base.size() * 4)) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_bits_desc), bits_desc.data(), bits_desc.size() * 4)) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_leaves), leaf_values, u32 ? 0 : static_cast<size_t>(n_leaves) * 4)) != cudaSuccess) {
         odf_model *raw = m.release();
         odf_free_model(raw);
         return e == cudaErrorMemoryAllocation ? fail(ODF_E_NOMEM, "device allocation failed")
@@ -764,6 +789,66 @@ odf_status odf_score_fm(const odf_model *m, const float *d_factors_fm, int64_t n
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
     return run_main(m, MODE_FUSED, d_factors_fm, n_docs, ld_fm, nullptr, nullptr, d_scores,
                     static_cast<cudaStream_t>(stream), nullptr, nullptr, true);
+}
+
+odf_status odf_bits_layout(const odf_model *m, int64_t n_docs, size_t *bytes, int64_t *n_binary)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (bytes) *bytes = static_cast<size_t>((n_docs + 31) / 32) * m->total_borders * 4;
+    if (n_binary) *n_binary = m->total_borders;
+    return ok();
+}
+
+odf_status odf_bits_from_bins(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                              uint32_t *d_words, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs == 0 || m->total_borders == 0) return ok();
+    if (!d_bins || !d_words) return fail(ODF_E_INVALID_ARG, "NULL buffer");
+    KParams p = base_params(m, m->apply);
+    p.n_docs = n_docs;
+    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.bins_in = d_bins;
+    p.bf_base = m->d_bf_base;
+    p.k_bin = m->total_borders;
+    p.words = d_words;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != m->device) cudaSetDevice(m->device);
+    cudaError_t e = launch_bits(m->depth, p, false, 0, static_cast<cudaStream_t>(stream));
+    if (prev != m->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "bits kernel");
+    return ok();
+}
+
+odf_status odf_apply_bits(const odf_model *m, const uint32_t *d_words, int64_t n_docs,
+                          float *d_scores, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_UNSUPPORTED, "bit-word apply: fp32-leaf models only");
+    if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    if (n_docs == 0) return ok();
+    if (!d_scores || (m->total_borders > 0 && !d_words)) return fail(ODF_E_INVALID_ARG, "NULL buffer");
+    const size_t smem = align_up(static_cast<uint64_t>(m->total_borders) * 4, 16) + kConsumerWarps * 32 * 4;
+    if (smem > static_cast<size_t>(m->max_smem))
+        return fail(ODF_E_UNSUPPORTED, "bit-word apply: %lld binary features do not fit shared memory",
+                    (long long)m->total_borders);
+    KParams p = base_params(m, m->apply);
+    p.n_docs = n_docs;
+    p.scores = d_scores;
+    p.k_bin = m->total_borders;
+    p.words = const_cast<uint32_t *>(d_words);
+    p.bits_desc = m->d_bits_desc;
+    p.leaves = m->d_leaves;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != m->device) cudaSetDevice(m->device);
+    cudaError_t e = launch_bits(m->depth, p, true, smem, static_cast<cudaStream_t>(stream));
+    if (prev != m->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "bits apply kernel");
+    return ok();
 }
 
 odf_status odf_score_u64(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,

@@ -76,6 +76,12 @@ struct KParams {
     uint8_t *lat_codes;      // [n_tiles][n_cols][128] 7-bit codes
     float *lat_partial;      // [n_tiles][splits][128]
     uint32_t *lat_counter;   // [n_tiles] tickets
+    // ---- NEXT-3 bit-packed condition words ----
+    const uint32_t *bf_base;   // [n_used + 1] first binary feature of each used factor
+    int64_t k_bin;             // number of binary features
+    uint32_t *words;           // [ceil(D/32)][k_bin]
+    const uint32_t *bits_desc; // [n_trees][depth] byte offset (kb * 4) of each level's word
+    const float *leaves;       // [n_trees << depth] original leaf order
     // ---- index export / fingerprint ----
     int64_t doc0, ndoc, tree0, ntree;
     uint16_t *idx_out;
@@ -88,6 +94,7 @@ cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid
                          cudaStream_t s);
 cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,
                            size_t smem_bin, size_t smem_apply, cudaStream_t s);
+cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cudaStream_t s);
 // Opt every kernel in to `smem` bytes of dynamic shared memory.
 cudaError_t prepare_kernels(int max_smem);
 // Number of co-resident CTAs per SM of a main kernel at `smem` bytes.

@@ -856,6 +856,100 @@ __global__ void __launch_bounds__(kConsumerThreads)
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-3: bit-packed ordered condition words (the paper's "ordered format",
+// §5.4: bit i <-> document i), one u32 per binary feature per 32
+// documents, built with __ballot_sync; and an apply that assembles each leaf index
+// from those words (§6.4).  Binary feature kb = (used factor u, border j),
+// numbered by ascending u then j; its bit for document i is (bin(x_i) <= j), i.e.
+// the node condition x < b_j itself.  Words: [ceil(D/32)][K_bin].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kConsumerThreads)
+    odf_bits_from_bins_kernel(const KParams p)
+{
+    const int64_t tile = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint8_t *bt = p.bins_in + tile * static_cast<int64_t>(p.n_used) * kTile;
+    for (int u = warp; u < p.n_used; u += kConsumerWarps) {
+        const uint32_t base = p.bf_base[u], m = p.bf_base[u + 1] - base;
+#pragma unroll 1
+        for (int q = 0; q < kTile / 32; ++q) {
+            const int64_t g = tile * (kTile / 32) + q;  // 32-document group
+            if (g * 32 >= p.n_docs) break;
+            const bool valid = g * 32 + lane < p.n_docs;  // padding documents: bit 0
+            const uint32_t b = valid ? bt[u * kTile + q * 32 + lane] : 0xffffffffu;
+            uint32_t *dst = p.words + g * p.k_bin + base;
+            for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+                uint32_t mine = 0;
+                const uint32_t nj = min(32u, m - j0);
+                for (uint32_t jj = 0; jj < nj; ++jj) {
+                    const uint32_t w = __ballot_sync(0xffffffffu, b <= j0 + jj);
+                    if (lane == static_cast<int>(jj)) mine = w;
+                }
+                if (static_cast<uint32_t>(lane) < nj) dst[j0 + lane] = mine;
+            }
+        }
+    }
+}
+
+// One CTA per 32-document group; lane = document; warp w sums trees t = w mod 16 in
+// ascending order and the 16 partials are combined in order: the same summation
+// order as the main path, so scores are bit-identical to odf_score.
+template <int DEPTH>
+__global__ void __launch_bounds__(kConsumerThreads)
+    odf_apply_bits_kernel(const KParams p)
+{
+    const int64_t g = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t *wg = p.words + g * p.k_bin;
+    for (int64_t k = tid; k < p.k_bin; k += kConsumerThreads) sst<uint32_t>(4u * k, wg[k]);
+    __syncthreads();
+    const uint32_t red = (4u * static_cast<uint32_t>(p.k_bin) + 15u) & ~15u;
+    float acc = 0.f;
+    for (int64_t t = warp; t < p.n_trees; t += kConsumerWarps) {
+        uint32_t idx = 0;
+#pragma unroll
+        for (int l = 0; l < DEPTH; ++l) {
+            const uint32_t w = lds_u32(__ldg(p.bits_desc + t * DEPTH + l));  // broadcast
+            idx |= ((w >> lane) & 1u) << l;
+        }
+        acc += __ldg(p.leaves + (t << DEPTH) + idx);
+    }
+    sst<float>(red + 4u * (warp * 32 + lane), acc);
+    __syncthreads();
+    if (tid < 32) {
+        float s = lds_f32(red + 4u * tid);
+#pragma unroll
+        for (int w = 1; w < kConsumerWarps; ++w) s += lds_f32(red + 4u * (w * 32 + tid));
+        const int64_t doc = g * 32 + tid;
+        if (doc < p.n_docs) p.scores[doc] = s;
+    }
+}
+
+template <int DEPTH>
+static const void *bits_fn()
+{
+    return reinterpret_cast<const void *>(&odf_apply_bits_kernel<DEPTH>);
+}
+
+cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cudaStream_t s)
+{
+    static const void *t[11] = {bits_fn<0>(), bits_fn<1>(), bits_fn<2>(), bits_fn<3>(),
+                                bits_fn<4>(), bits_fn<5>(), bits_fn<6>(), bits_fn<7>(),
+                                bits_fn<8>(), bits_fn<9>(), bits_fn<10>()};
+    KParams pc = p;
+    void *args[] = {&pc};
+    if (!apply)
+        return cudaLaunchKernel(reinterpret_cast<const void *>(&odf_bits_from_bins_kernel),
+                                dim3(static_cast<unsigned>(p.n_tiles)), dim3(kConsumerThreads), args, 0, s);
+    if (depth < 0 || depth > 10) return cudaErrorInvalidValue;
+    const void *f = t[depth];
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernel(f, dim3(static_cast<unsigned>((p.n_docs + 31) / 32)), dim3(kConsumerThreads),
+                            args, smem, s);
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 template <int MODE, int DEPTH, bool U32>

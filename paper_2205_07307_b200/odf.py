@@ -95,6 +95,12 @@ def lib():
     L.odf_binarize_fm.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
     L.odf_score_fm.restype = ctypes.c_int
     L.odf_score_fm.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+    L.odf_bits_layout.restype = ctypes.c_int
+    L.odf_bits_layout.argtypes = [_vp, _i64, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_i64)]
+    L.odf_bits_from_bins.restype = ctypes.c_int
+    L.odf_bits_from_bins.argtypes = [_vp, _vp, _i64, _vp, _vp]
+    L.odf_apply_bits.restype = ctypes.c_int
+    L.odf_apply_bits.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.odf_score_u64.restype = ctypes.c_int
     L.odf_score_u64.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _vp]
     L.odf_apply_u64.restype = ctypes.c_int
@@ -131,7 +137,7 @@ ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_mode
                "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host",
                "odf_latency_workspace_bytes", "odf_score_latency", "odf_load_model_ex",
                "odf_score_u64", "odf_apply_u64", "odf_load_model_paper", "odf_binarize_fm",
-               "odf_score_fm")
+               "odf_score_fm", "odf_bits_layout", "odf_bits_from_bins", "odf_apply_bits")
 
 
 def _check(status: int):
@@ -327,6 +333,28 @@ class Model:
             out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
         _check(lib().odf_score_fm(self._h, _ptr(xt), int(n_docs), ld, _ptr(out),
                                   _stream(stream, self._dev())))
+        return out
+
+    # -- NEXT-3: bit-packed ordered condition words --------------------------------
+    def bits_layout(self, n_docs: int):
+        nb = ctypes.c_size_t()
+        k = _i64()
+        _check(lib().odf_bits_layout(self._h, int(n_docs), ctypes.byref(nb), ctypes.byref(k)))
+        return int(nb.value), int(k.value)
+
+    def bits_from_bins(self, bins: torch.Tensor, n_docs: int, out=None, stream=None):
+        nbytes, k = self.bits_layout(n_docs)
+        if out is None:
+            out = torch.empty(max(nbytes // 4, 1), dtype=torch.int32, device=self._dev())
+        _check(lib().odf_bits_from_bins(self._h, _ptr(bins), int(n_docs), _ptr(out),
+                                        _stream(stream, self._dev())))
+        return out
+
+    def apply_bits(self, words: torch.Tensor, n_docs: int, out=None, stream=None):
+        if out is None:
+            out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
+        _check(lib().odf_apply_bits(self._h, _ptr(words), int(n_docs), _ptr(out),
+                                    _stream(stream, self._dev())))
         return out
 
     def score_host(self, x, out=None, chunk_docs: int = 65536, stream=None):

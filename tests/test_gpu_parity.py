@@ -449,3 +449,27 @@ def test_deterministic_over_many_tiles(name, n_docs, n_trees):
         assert torch.equal(m.apply(bins, n_docs).view(torch.int32), ref.view(torch.int32))
     torch.cuda.synchronize()
     m.close()
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: bit-packed ordered condition words (ballot) and the apply over them
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n_docs,n_trees", [("c1", 1024, None), ("c1", 33, None),
+                                                 ("c2", 5000, 300), ("c4", 1000, 64)])
+def test_condition_words_and_bits_apply(name, n_docs, n_trees):
+    import torch
+    case = synth.make_case(name, n_docs=n_docs, n_trees=n_trees)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    bins = m.binarize(x)
+    words = m.bits_from_bins(bins, n_docs)
+    nbytes, k = m.bits_layout(n_docs)
+    per, flat, counts, offs = oracle.borders(case.feature_index, case.thresholds, case.n_features)
+    want = oracle.condition_words(case.x, case.n_features, flat, counts, offs)
+    got = words[: nbytes // 4].cpu().numpy().view(np.uint32).reshape(-1, k)
+    assert np.array_equal(got, want)
+    s_bits = m.apply_bits(words, n_docs).cpu().numpy()
+    s_main = m.score(x).cpu().numpy()
+    assert np.array_equal(s_bits.view(np.uint32), s_main.view(np.uint32))
+    torch.cuda.synchronize()
+    m.close()

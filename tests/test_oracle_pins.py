@@ -344,3 +344,18 @@ def test_paper_native_apply_matches_brute_force():
             cb += h
             lb += 1 << h
         assert int(got[i]) == total
+
+
+def test_condition_words_ordered_bits():
+    # bit i of a word <-> document i; each bit is the raw condition x < border
+    c = synth.tiny_case(seed=81, n_docs=70, n_features=5, n_trees=20, depth=3, pool=6)
+    per, flat, counts, offs = oracle.borders(c.feature_index, c.thresholds, 5)
+    w = oracle.condition_words(c.x, 5, flat, counts, offs)
+    kb = 0
+    for f in range(5):
+        for j in range(counts[f]):
+            for i in range(70):
+                bit = (int(w[i // 32, kb]) >> (i % 32)) & 1
+                assert bit == int(np.float32(c.x[i, f]) < per[f][j])
+            kb += 1
+    assert w.shape == (3, int(counts.sum()))
