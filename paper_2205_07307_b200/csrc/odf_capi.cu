@@ -128,11 +128,13 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
         slot = align_up(m.chunk_bytes, 1024);
         smax = 4;
     } else {
-        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(unit, 1024));
+        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(2u * unit, 1024));
         smax = 8;
     }
     const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
     const int64_t fixed = static_cast<int64_t>(bins_region) + bars;
+    if (mode == MODE_FUSED && (avail - fixed) / slot < 2)  // fall back to one sub-tile per slot
+        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(unit, 1024));
     pl.stages = std::min<int64_t>(smax, (avail - fixed) / slot);
     if (pl.stages < 2) {
         char b[256];
@@ -549,7 +551,20 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     // ---- tree chunks: descriptors + reversed leaf tables ----
     const int dstride = desc_stride(depth);
     m->table_stride = static_cast<uint32_t>(table_stride(depth));
-    m->tc = trees_per_chunk(depth);
+    // chunk size: ~20 KB, or about two factor sub-tiles (16.5 KB + borders each) so
+    // a ring slot carries 2 sub-tiles in phase A and >= 64 trees in phase B
+    {
+        int max_smem = 0;
+        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
+        const int64_t bins = std::max<int64_t>(align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024),
+                                               2 * kRedBytes);
+        const int64_t room = static_cast<int64_t>(max_smem) - 1024 - 1024 - bins;  // for >= 2 slots
+        uint32_t target = 20480u;
+        if (room / 2 >= static_cast<int64_t>(align_up(2u * unit, 1024))) target = 2u * unit;
+        const uint32_t per = static_cast<uint32_t>(dstride) + m->table_stride;
+        m->tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, target / (16u * per)));
+    }
     m->desc_bytes = align_up(static_cast<uint64_t>(m->tc) * dstride, 256);
     m->chunk_bytes = m->desc_bytes + static_cast<uint32_t>(m->tc) * m->table_stride;
     m->n_tchunks = static_cast<int32_t>((n_trees + m->tc - 1) / m->tc);

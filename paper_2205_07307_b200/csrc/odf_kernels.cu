@@ -483,11 +483,11 @@ struct Acc<true> {
 
 template <int DEPTH, bool U32>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
-                                            int warp, Acc<U32> &acc)
+                                            int warp, int nk, Acc<U32> &acc)
 {
-    constexpr int TC = trees_per_chunk(DEPTH);  // chunks are padded to TC trees
-#pragma unroll
-    for (int k = 0; k < TC / kConsumerWarps; ++k) {
+    // chunks hold nk * 16 trees (the last one padded with zero-answer trees)
+#pragma unroll 2
+    for (int k = 0; k < nk; ++k) {
         const int i = warp + k * kConsumerWarps;
         const uint32_t d = chunk + i * desc_stride(DEPTH);
         const uint32_t tb = chunk + desc_bytes + i * table_stride(DEPTH);
@@ -670,7 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
             mbar_wait(full, ph);
-            apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, p.desc_bytes, lane_bins, warp, acc);
+            apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, p.desc_bytes, lane_bins, warp,
+                                    p.tc / kConsumerWarps, acc);
             acc.pin(pin_scratch);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty);
@@ -830,7 +831,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         for (uint32_t k = tid; k < p.chunk_bytes / 16; k += kConsumerThreads)
             sts_v4u(chunk + 16 * k, __ldg(src + k));
         __syncthreads();
-        apply_chunk<DEPTH, false>(chunk, p.desc_bytes, lane_bins, warp, acc);
+        apply_chunk<DEPTH, false>(chunk, p.desc_bytes, lane_bins, warp, p.tc / kConsumerWarps, acc);
     }
     acc.to_red(red, warp, lane);
     __syncthreads();
