@@ -200,9 +200,16 @@ def run_ours(args):
     import synth
     from paper_2205_07307_b200 import Model
 
-    case = _workload(args.config, rank)
-    model = Model(case.feature_index, case.thresholds, case.leaf_values, case.depth,
-                  case.n_features, device=local)
+    tree_shard = args.shard == "trees"
+    case = _workload(args.config, 0 if tree_shard else rank)
+    if tree_shard:  # rank r holds trees [r*T/W, (r+1)*T/W) and scores every document
+        from paper_2205_07307_b200.parallel import tree_shard as _shard
+        fi, th, lv, _ = _shard(case.feature_index, case.thresholds, case.leaf_values, case.depth,
+                               ws, rank)
+        model = Model(fi, th, lv, case.depth, case.n_features, device=local)
+    else:
+        model = Model(case.feature_index, case.thresholds, case.leaf_values, case.depth,
+                      case.n_features, device=local)
     info = model.info
     x = torch.from_numpy(case.x).to(dev)
     n = case.n_docs
@@ -211,6 +218,8 @@ def run_ours(args):
 
     def step():
         model.score(x, out=out, stream=stream)
+        if tree_shard and ws > 1:  # one NCCL all-reduce of the fp32 partial scores
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
 
     for _ in range(args.warmup):
         step()
@@ -264,13 +273,23 @@ def run_ours(args):
     # ---- end to end through the public API from pinned host memory ----
     xh = torch.from_numpy(case.x).pin_memory()
     sh = torch.empty(n, dtype=torch.float32).pin_memory()
-    model.score_host(xh, out=sh, chunk_docs=args.e2e_chunk)
+
+    def e2e_step():
+        if tree_shard and ws > 1:  # H2D, shard scores, NCCL all-reduce, D2H
+            x.copy_(xh, non_blocking=True)
+            step()
+            sh.copy_(out, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        else:
+            model.score_host(xh, out=sh, chunk_docs=args.e2e_chunk)
+
+    e2e_step()
     k_e2e = max(1, min(args.steps, args.e2e_steps))
     if ws > 1:
         dist.barrier()
     t_e = time.perf_counter()
     for _ in range(k_e2e):
-        model.score_host(xh, out=sh, chunk_docs=args.e2e_chunk)
+        e2e_step()
     e2e_s = time.perf_counter() - t_e
     if ws > 1:
         t = torch.tensor([e2e_s], device=dev)
@@ -280,7 +299,7 @@ def run_ours(args):
     line = None
     if rank == 0:
         peak, peak_kind = _peaks()
-        docs_total = n * args.steps * ws
+        docs_total = n * args.steps * (1 if tree_shard else ws)
         value = docs_total / (total_ms / 1000.0)
         alg_bytes = n * (4 * info["n_used_features"] + 4)  # fused = 4*F_used + 4
         achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
@@ -288,14 +307,15 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "docs/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong" if tree_shard else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": synth.WORKLOAD_NAMES[args.config], "n_docs": n,
                        "n_features": case.n_features, "n_trees": case.n_trees,
                        "depth": case.depth, "used_features": info["n_used_features"],
                        "path": "fused odf_score",
                        "l2": "inputs larger than L2 (%.0f MB > 126 MB); no flush" % (case.x.nbytes / 1e6),
-                       "parallelism": f"doc-shard x{ws}"},
+                       "parallelism": (f"tree-shard x{ws} + NCCL all-reduce" if tree_shard
+                                       else f"doc-shard x{ws}")},
             "doc_trees_per_s": value * case.n_trees,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
@@ -328,6 +348,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shard", default="docs", choices=["docs", "trees"],
+                    help="multi-GPU: document sharding (weak scaling) or tree sharding + NCCL "
+                         "all-reduce of fp32 partials (strong scaling)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunk", type=int, default=16384)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
