@@ -146,6 +146,7 @@ typedef struct {
     int32_t smem_fused;         /* dynamic shared memory per CTA of the fused kernel, bytes */
     int32_t num_sms;
     int32_t leaf_type;          /* ODF_LEAF_F32 / ODF_LEAF_U32 */
+    int32_t bord_stride;        /* max bytes of one 32-factor sub-tile's border arrays */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);

@@ -58,6 +58,7 @@ odf_status cuda_fail(cudaError_t e, const char *what)
 }
 
 uint32_t skew_h(uint32_t p) { return p + (p >> 5); }  // as skew() in odf_kernels.cu
+constexpr uint32_t kSplitFlagH = 0x10u;                 // as kSplitFlag in odf_kernels.cu
 uint32_t align_up(uint64_t v, uint64_t a) { return static_cast<uint32_t>((v + a - 1) / a * a); }
 
 struct Plan {
@@ -112,8 +113,8 @@ namespace {
 // ----------------------------------------------------------------------------
 bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
 {
-    const uint32_t cols = (mode == MODE_BINARIZE) ? m.n_used : m.n_cols;
-    const uint32_t bins = align_up(static_cast<uint64_t>(cols) * kTile, 1024);
+    // code columns + the trash column (stores of unused pair slots)
+    const uint32_t bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile, 1024);
     const uint32_t red_bytes = m.leaf_u32 ? 2 * kRedBytes : kRedBytes;
     const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes);
     const uint32_t bars = align_up(160 + 8u * m.n_fchunks, 128);  // barriers, scratch, bchunk copy
@@ -139,7 +140,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
     if (pl.stages < 2) {
         char b[256];
         snprintf(b, sizeof b,
-                 "shared memory: %u code columns x 128 B + 2 x %u B slots do not fit %d B", cols,
+                 "shared memory: %d code columns x 128 B + 2 x %u B slots do not fit %d B", m.n_cols,
                  slot, m.max_smem);
         why = b;
         return false;
@@ -207,6 +208,7 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.n_split = m->n_split;
     p.n_used = m->n_used;
     p.n_cols = m->n_cols;
+    p.code_stride = static_cast<int64_t>(m->n_cols + 1) * kTile;
     p.off_bins = pl.off_bins;
     p.off_ring = pl.off_ring;
     p.off_red = pl.off_red;
@@ -473,60 +475,47 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     m->n_split = static_cast<int32_t>(splits.size());
     m->n_cols = m->n_used + m->n_split;
 
-    // ---- factor metadata + border arrays (binarize; kinds in odf_internal.h) ----
+    // ---- factor metadata + border arrays (binarize; layout in odf_internal.h) ----
+    // Pairs (f, f+1), f even, share one code path: LIN4 if both have <= 4 borders,
+    // else BIN(L) with the pair's L.  Each array is npad copies of -inf followed by
+    // the factor's sorted borders (bin = count - npad).
     m->n_fchunks = (n_features + kFSub - 1) / kFSub;
-    std::vector<uint4> fmeta(static_cast<size_t>(m->n_fchunks) * kFSub, make_uint4(0, 0, 0, kNoCol));
+    const uint32_t trash = static_cast<uint32_t>(m->n_cols) * kTile;  // column of discarded stores
+    std::vector<uint4> fmeta(static_cast<size_t>(m->n_fchunks) * kFSub, make_uint4(0, 0, trash, trash));
     std::vector<float> bflat;
     auto ceil_log2p1 = [](uint32_t mm) {
         uint32_t L = 0;
         while (((1u << L) - 1u) < mm) ++L;  // smallest L with 2^L - 1 >= m
         return L;
     };
-    // pairs (f, f+1), f even: LIN4 if both have <= 4 borders, else BIN padded to the pair's L
-    std::vector<uint32_t> kind(fmeta.size(), 0), Lof(fmeta.size(), 0);
+    auto n_borders = [&](size_t f) -> uint32_t {
+        return f < static_cast<size_t>(n_features) ? static_cast<uint32_t>(borders[f].size()) : 0u;
+    };
     for (size_t f = 0; f < fmeta.size(); f += 2) {
-        const uint32_t ma = f < static_cast<size_t>(n_features) ? static_cast<uint32_t>(borders[f].size()) : 0;
-        const uint32_t mb = f + 1 < static_cast<size_t>(n_features) ? static_cast<uint32_t>(borders[f + 1].size()) : 0;
+        const uint32_t ma = n_borders(f), mb = n_borders(f + 1);
         if (ma == 0 && mb == 0) continue;
-        const uint32_t k = std::max(ma, mb) <= 4 ? 1u : 2u;
-        const uint32_t L = k == 2 ? ceil_log2p1(std::max(ma, mb)) : 0u;
-        kind[f] = kind[f + 1] = k;
-        Lof[f] = Lof[f + 1] = L;
-    }
-    for (int32_t f : m->used_ids) {
-        const auto &b = borders[f];
-        const uint32_t mm = static_cast<uint32_t>(b.size());
-        const uint32_t off = static_cast<uint32_t>(bflat.size());
-        if (kind[f] == 1) {
-            bflat.resize(off + 4, INFINITY);
-            for (uint32_t j = 0; j < mm; ++j) bflat[off + j] = b[j];
-        } else {
-            const uint32_t n_pad = (1u << Lof[f]) - 1u;
-            bflat.resize(off + skew_h(n_pad - 1u) + 1u, INFINITY);
-            for (uint32_t pidx = 0; pidx < n_pad; ++pidx)
-                bflat[off + skew_h(pidx)] = pidx < mm ? b[pidx] : INFINITY;
+        const bool lin = std::max(ma, mb) <= 4;
+        const uint32_t L = lin ? 0u : ceil_log2p1(std::max(ma, mb));
+        const uint32_t cls = lin ? 1u : L + 1u;
+        const uint32_t n_ent = lin ? 4u : (1u << L) - 1u;
+        for (size_t g = f; g < f + 2; ++g) {
+            const uint32_t mm = n_borders(g);
+            if (mm == 0) continue;
+            const auto &b = borders[g];
+            const uint32_t off = static_cast<uint32_t>(bflat.size());
+            const uint32_t npad = n_ent - mm;
+            bflat.resize(off + skew_h(n_ent - 1u) + 1u, -INFINITY);
+            for (uint32_t pidx = 0; pidx < n_ent; ++pidx)
+                bflat[off + skew_h(pidx)] = pidx < npad ? -INFINITY : b[pidx - npad];
+            while (bflat.size() % 4) bflat.push_back(-INFINITY);  // 16-byte aligned arrays
+            const bool split = mm > 127;
+            fmeta[g] = make_uint4(off, cls | (split ? kSplitFlagH : 0u) | (npad << 16),
+                                  static_cast<uint32_t>(used_of[g]) * kTile,
+                                  split ? static_cast<uint32_t>(colB_of[g]) * kTile : trash);
         }
-        while (bflat.size() % 4) bflat.push_back(INFINITY);  // 16-byte aligned arrays
-        fmeta[f] = make_uint4(off, kind[f] | (Lof[f] << 8) | (mm << 16),
-                              static_cast<uint32_t>(used_of[f]) * kTile,
-                              colB_of[f] >= 0 ? static_cast<uint32_t>(colB_of[f]) * kTile : kNoCol);
-    }
-    // SIMPLE pairs (kind bit 0x10): both factors used and neither has a second column,
-    // so the kernel stores the bin directly as the code
-    for (size_t f = 0; f + 1 < fmeta.size(); f += 2) {
-        const bool ua = f < static_cast<size_t>(n_features) && !borders[f].empty();
-        const bool ub = f + 1 < static_cast<size_t>(n_features) && !borders[f + 1].empty();
-        if (ua && ub && borders[f].size() <= 127 && borders[f + 1].size() <= 127) {
-            fmeta[f].y |= 0x10u;
-            fmeta[f + 1].y |= 0x10u;
-        }
-    }
-    // the unused factor of a mixed pair searches its partner's array and stores nothing
-    for (size_t f = 0; f + 1 < fmeta.size(); f += 2) {
-        const bool ua = f < static_cast<size_t>(n_features) && !borders[f].empty();
-        const bool ub = f + 1 < static_cast<size_t>(n_features) && !borders[f + 1].empty();
-        if (ua && !ub) fmeta[f + 1] = make_uint4(fmeta[f].x, fmeta[f].y & 0xffffu, kNoCol, kNoCol);
-        if (ub && !ua) fmeta[f] = make_uint4(fmeta[f + 1].x, fmeta[f + 1].y & 0xffffu, kNoCol, kNoCol);
+        // the unused factor of a mixed pair searches its partner's array, stores to trash
+        if (ma == 0) fmeta[f] = make_uint4(fmeta[f + 1].x, fmeta[f + 1].y & ~kSplitFlagH, trash, trash);
+        if (mb == 0) fmeta[f + 1] = make_uint4(fmeta[f].x, fmeta[f].y & ~kSplitFlagH, trash, trash);
     }
     m->border_floats = static_cast<int32_t>(bflat.size());
     // per sub-tile border ranges; fmeta.x becomes relative to its sub-tile's range
@@ -534,10 +523,9 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     for (int32_t c = 0; c < m->n_fchunks; ++c) {
         uint32_t lo = UINT32_MAX, hi = 0;
         for (int32_t f = c * kFSub; f < (c + 1) * kFSub; ++f) {
-            if ((fmeta[f].y & 0xfu) == 0) continue;
-            const uint32_t kf = fmeta[f].y & 0xfu;
-            const uint32_t L = (fmeta[f].y >> 8) & 0xffu;
-            const uint32_t len = kf == 1 ? 4u : skew_h((1u << L) - 2u) + 1u;
+            const uint32_t cls = fmeta[f].y & 0xfu;
+            if (cls == 0) continue;
+            const uint32_t len = cls == 1 ? 4u : skew_h((1u << (cls - 1)) - 2u) + 1u;
             lo = std::min(lo, fmeta[f].x);
             hi = std::max(hi, (fmeta[f].x + len + 3u) & ~3u);
         }
@@ -557,7 +545,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         int max_smem = 0;
         cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
-        const int64_t bins = std::max<int64_t>(align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024),
+        const int64_t bins = std::max<int64_t>(align_up(static_cast<uint64_t>(m->n_cols + 1) * kTile, 1024),
                                                2 * kRedBytes);
         const int64_t room = static_cast<int64_t>(max_smem) - 1024 - 1024 - bins;  // for >= 2 slots
         uint32_t target = 20480u;
@@ -696,6 +684,7 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->smem_fused = static_cast<int32_t>(m->fused.smem);
     info->num_sms = m->num_sms;
     info->leaf_type = m->leaf_u32 ? ODF_LEAF_U32 : ODF_LEAF_F32;
+    info->bord_stride = static_cast<int32_t>(m->bord_stride);
     return ok();
 }
 
@@ -963,7 +952,7 @@ static void lat_layout(const odf_model *m, int64_t n_docs, int sp, size_t off[4]
     const int64_t tiles = (n_docs + kTile - 1) / kTile;
     auto a256 = [](size_t v) { return (v + 255) / 256 * 256; };
     off[0] = 0;
-    off[1] = a256(static_cast<size_t>(tiles) * m->n_cols * kTile);
+    off[1] = a256(static_cast<size_t>(tiles) * (m->n_cols + 1) * kTile);
     off[2] = off[1] + a256(static_cast<size_t>(tiles) * sp * kTile * 4);
     off[3] = off[2] + a256(static_cast<size_t>(tiles) * 4);
 }

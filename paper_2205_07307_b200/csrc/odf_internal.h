@@ -37,12 +37,13 @@ enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 // Per-launch parameters (passed by value; all pointers are device pointers).
 struct KParams {
     // ---- binarization (stage 1) ----
-    const uint4 *fmeta;     // [n_fchunks*32] per raw factor: {border_off (floats, 16 B aligned),
-                            //  kind | L<<8 | m<<16, colA*128, colB*128 or kNoCol}
-                            //  kind: 0 unused, 1 LIN4, 2 LIN8, 3 BIN, 4 PAIR(first), 5 PAIRED
-    const float *borders;   // per used factor: LIN4/LIN8 -> 4/8 sorted borders padded with
-                            // +inf; BIN/PAIR -> sorted borders padded to 2^L-1 with +inf,
-                            // stored skewed (position p at p + (p >> 5))
+    const uint4 *fmeta;     // [n_fchunks*32] per raw factor: {array offset (floats, relative to
+                            //  its sub-tile's border block, 16 B aligned), cls | flags | npad<<16,
+                            //  colA*128, colB*128}; cls 0 unused, 1 LIN4, L+1 BIN(L); flag 0x10
+                            //  split (> 127 borders); unused slots of a pair: trash column
+    const float *borders;   // per used factor: npad x -inf then its m sorted borders; LIN4
+                            // arrays have 4 entries, BIN(L) arrays 2^L-1 entries stored skewed
+                            // (position p at p + (p >> 5))
     const uint2 *bchunk;    // [n_fchunks] {byte offset into borders, bytes} of each sub-tile's
                             // border arrays (fmeta.x is relative to that offset)
     int32_t n_fchunks;      // ceil(n_features / 32), 0 if no used factor
@@ -73,7 +74,8 @@ struct KParams {
     int32_t stages;
     int32_t fsub_per_job;    // factor sub-tiles per job (tiles, then metas, then borders)
     // ---- latency path (K4) workspace ----
-    uint8_t *lat_codes;      // [n_tiles][n_cols][128] 7-bit codes
+    uint8_t *lat_codes;      // [n_tiles][n_cols + 1][128] 7-bit codes (+ trash column)
+    int64_t code_stride;     // bytes per tile of a global code block: (n_cols + 1) * 128
     float *lat_partial;      // [n_tiles][splits][128]
     uint32_t *lat_counter;   // [n_tiles] tickets
     // ---- NEXT-3 bit-packed condition words ----

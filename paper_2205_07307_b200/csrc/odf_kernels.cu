@@ -27,6 +27,10 @@
 
 #include "odf_internal.h"
 
+#ifndef ODF_DIAG
+#define ODF_DIAG 0  // diagnostics builds (tools/, never the product): see build.build_variant
+#endif
+
 namespace odf {
 
 // ---------------------------------------------------------------------------
@@ -71,6 +75,31 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
     return d;
 }
+// Loads by ABSOLUTE shared-window address (stage 1: read-only TMA-slot data, so
+// volatile asm keeps them after the slot's mbarrier wait; ptxas still schedules
+// them and folds constant offsets into the LDS immediate).
+__device__ __forceinline__ float ldsa_f32(uint32_t a)
+{
+    float r;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ float4 ldsa_v4f(uint32_t a)
+{
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint4 ldsa_v4u(uint32_t a)
+{
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(a));
+    return r;
+}
 __device__ __forceinline__ void named_bar_consumers()
 {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerThreads) : "memory");
@@ -95,9 +124,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "ODF_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra ODF_WAIT_%=;\n}\n" ::"r"(sabs(bar)),
-        "r"(parity)
+        "r"(parity), "n"(0x989680)  // suspend-time hint: the warp sleeps instead of spinning
         : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init()
@@ -146,26 +175,29 @@ __device__ __forceinline__ void bulk_wait_all()
 // ---------------------------------------------------------------------------
 // The TMA box lands with SWIZZLE_128B: 16-byte chunk q of row r sits at chunk
 // q ^ (r & 7), so warp-wide reads of one chunk (32 rows) are conflict-free.
-// Warp w handles documents (w&3)*32 + lane and the factor quads (w>>2) and
-// (w>>2)+4 of the sub-tile, i.e. 4 pairs of adjacent factors (2 per LDS.64).
+// A warp handles one factor quad q (the 4 factors of chunk q, read with one
+// LDS.128 per document) for NDL documents per lane: dbase + lane + 32n.
 //
-// bin(x) = #{j : !(x < b_j)}.  Each pair of adjacent factors is
-// evaluated with one straight-line code path chosen by the model compiler
-// (fmeta.y = kind | L<<8 | m<<16, identical kind/L for both factors of a pair):
-//   LIN4  both m <= 4: count !(x < b_j) over 4 borders padded with +inf
-//         (warp-uniform broadcast loads, no dependent chain);
-//   BIN   branchless search over the sorted borders padded to 2^L - 1 with
-//         +inf, both factors padded to the pair's L and searched interleaved
-//         (two independent chains per lane); arrays are stored skewed
-//         (position p at p + (p >> 5)) so the lanes of one step hit distinct banks.
-// For every x the predicate !(x < b) is a prefix of the padded sorted array
-// (NaN and +inf: the whole array), so every count is min(count, m).
-// An unused factor of a pair searches its partner's array and stores nothing.
-enum : uint32_t { BK_SKIP = 0, BK_LIN4 = 1, BK_BIN = 2 };
+// bin(x) = #{j : !(x < b_j)}.  The quad is two pairs of adjacent
+// factors; both factors of a pair share one code path chosen by the model
+// compiler (fmeta.y & 0xf, warp-uniform):
+//   LIN4  both m <= 4: count !(x < e_j) over 4 entries (one broadcast LDS.128
+//         per factor, no dependent chain);
+//   BIN L branchless search over a sorted array of 2^L - 1 entries, stored skewed
+//         (position p at p + (p >> 5)) so the lanes of one step hit distinct banks;
+//         the pair's 2*NDL chains run interleaved.
+// Every array is the factor's sorted borders PRECEDED by npad = (length - m)
+// copies of -inf.  !(x < -inf) holds for every x (NaN included), so the count over
+// the padded array is exactly npad + bin(x): bin = count - npad, no clamping.
+// An unused factor of a pair searches its partner's array and stores into the
+// trash column; factors with > 127 borders (L = 8) also store a second code
+// column in the fused/latency paths (split flag).
+enum : uint32_t { CLS_SKIP = 0, CLS_LIN4 = 1 };  // cls >= 2: BIN with L = cls - 1
+constexpr uint32_t kSplitFlag = 0x10u;
 
 __host__ __device__ constexpr uint32_t skew(uint32_t p) { return p + (p >> 5); }
 
-// all-ones if !(x < b) (unordered or >=: NaN counts), else 0
+// 0xffffffff if !(x < b) (unordered or >=: NaN counts), else 0
 __device__ __forceinline__ uint32_t not_less_mask(float x, float b)
 {
     uint32_t r;
@@ -179,41 +211,9 @@ __device__ __forceinline__ void add_if_not_less(uint32_t &v, float x, float b, u
         : "+r"(v)
         : "f"(x), "f"(b), "r"(inc));
 }
-__device__ __forceinline__ uint32_t ge4(float x, float4 b)
-{
-    uint32_t c = 0;
-    add_if_not_less(c, x, b.x, 1u);
-    add_if_not_less(c, x, b.y, 1u);
-    add_if_not_less(c, x, b.z, 1u);
-    add_if_not_less(c, x, b.w, 1u);
-    return c;
-}
-
-// One step of the branchless search for 4 independent chains (2 factors x 2 docs).
-template <int L>
-__device__ __forceinline__ void search4(const float x[4], uint32_t pos[4])
-{
-#pragma unroll
-    for (int st = L - 1; st >= 0; --st) {
-        const uint32_t s = 1u << st;
-        float b[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) b[c] = lds_f32(pos[c] + 4u * skew(s - 1));
-#pragma unroll
-        for (int c = 0; c < 4; ++c) add_if_not_less(pos[c], x[c], b[c], 4u * (s + (s >> 5)));
-    }
-}
-
-template <int L>
-__device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t pos0, uint32_t m)
-{
-    uint32_t idx = (pos - pos0) >> 2;
-    if (L > 5) idx -= idx / 33u;  // unskew (idx < 264)
-    return min(idx, m);
-}
 
 // Where the bins / codes of a tile go: shared memory (fused, binarize) or a
-// global [n_cols][128] block (latency path).
+// global [n_cols + 1][128] block (latency path).
 struct SmemSink {
     uint32_t base;
     __device__ __forceinline__ void st(uint32_t off, uint32_t v) const { sts_u8(base + off, v); }
@@ -226,127 +226,146 @@ struct GmemSink {
     }
 };
 
-template <bool CODES, class Sink>
-__device__ __forceinline__ void store_bin(const Sink &bins, const uint4 &m, int doc, uint32_t bin)
+template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void store_bins(const Sink &s, const uint4 &m, uint32_t d0,
+                                           const uint32_t (&bin)[NDL])
 {
-    if (m.z == kNoCol) return;  // unused factor of a pair
-    if (CODES) {
-        bins.st(m.z + doc, min(bin, 127u));
-        if (m.w != kNoCol) bins.st(m.w + doc, max(bin, 127u) - 127u);
+    if (CODES && (m.y & kSplitFlag)) {  // warp-uniform; 7-bit code columns A and B
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) {
+            s.st(m.z + d0 + 32 * n, min(bin[n], 127u));
+            s.st(m.w + d0 + 32 * n, max(bin[n], 127u) - 127u);
+        }
     } else {
-        bins.st(m.z + doc, bin);
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) s.st(m.z + d0 + 32 * n, bin[n]);
     }
 }
 
-// Store of a SIMPLE pair (both factors used, <= 127 borders): the bin is its own code.
-template <class Sink>
-__device__ __forceinline__ void store_simple(const Sink &bins, const uint4 &m, int doc, uint32_t bin)
+template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void lin4_pair(const float (&xa)[NDL], const float (&xb)[NDL],
+                                          const uint4 &ma, const uint4 &mb, uint32_t bord,
+                                          const Sink &s, uint32_t d0)
 {
-    bins.st(m.z + doc, bin);
+    const float4 ea = ldsa_v4f(bord + ma.x * 4u), eb = ldsa_v4f(bord + mb.x * 4u);
+    const uint32_t na = 0u - (ma.y >> 16), nb = 0u - (mb.y >> 16);  // -npad
+    uint32_t ra[NDL], rb[NDL];
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        ra[n] = na;
+        rb[n] = nb;
+        add_if_not_less(ra[n], xa[n], ea.x, 1u);
+        add_if_not_less(rb[n], xb[n], eb.x, 1u);
+        add_if_not_less(ra[n], xa[n], ea.y, 1u);
+        add_if_not_less(rb[n], xb[n], eb.y, 1u);
+        add_if_not_less(ra[n], xa[n], ea.z, 1u);
+        add_if_not_less(rb[n], xb[n], eb.z, 1u);
+        add_if_not_less(ra[n], xa[n], ea.w, 1u);
+        add_if_not_less(rb[n], xb[n], eb.w, 1u);
+    }
+    store_bins<NDL, CODES>(s, ma, d0, ra);
+    store_bins<NDL, CODES>(s, mb, d0, rb);
 }
 
-// x = {a@doc0, a@doc1, b@doc0, b@doc1}
-template <bool CODES, int L, class Sink, bool SIMPLE>
-__device__ __forceinline__ void bin_pair(const float x[4], const uint4 &ma, const uint4 &mb,
-                                         uint32_t bord, const Sink &bins, int d0, int d1)
+template <int L>
+__device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t base, uint32_t npad)
+{
+    if constexpr (L <= 5) {
+        return (pos - (base + 4u * npad)) >> 2;  // count >= npad always
+    } else {
+        uint32_t idx = (pos - base) >> 2;
+        idx -= idx / 33u;  // unskew (idx < 264)
+        return idx - npad;
+    }
+}
+
+template <int L, int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void bin_pair(const float (&xa)[NDL], const float (&xb)[NDL],
+                                         const uint4 &ma, const uint4 &mb, uint32_t bord,
+                                         const Sink &s, uint32_t d0)
 {
     const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
-    uint32_t pos[4] = {a0, a0, b0, b0};
-    search4<L>(x, pos);
-    const uint32_t r0 = pos_to_bin<L>(pos[0], a0, ma.y >> 16), r1 = pos_to_bin<L>(pos[1], a0, ma.y >> 16);
-    const uint32_t r2 = pos_to_bin<L>(pos[2], b0, mb.y >> 16), r3 = pos_to_bin<L>(pos[3], b0, mb.y >> 16);
-    if (SIMPLE) {
-        store_simple(bins, ma, d0, r0);
-        store_simple(bins, ma, d1, r1);
-        store_simple(bins, mb, d0, r2);
-        store_simple(bins, mb, d1, r3);
-    } else {
-        store_bin<CODES, Sink>(bins, ma, d0, r0);
-        store_bin<CODES, Sink>(bins, ma, d1, r1);
-        store_bin<CODES, Sink>(bins, mb, d0, r2);
-        store_bin<CODES, Sink>(bins, mb, d1, r3);
+    uint32_t pa[NDL], pb[NDL];
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        pa[n] = a0;
+        pb[n] = b0;
     }
-}
-
-template <bool CODES, class Sink, bool SIMPLE>
-__device__ __forceinline__ void pair_dispatch_k(const float x[4], const uint4 &ma, const uint4 &mb,
-                                                uint32_t bord, const Sink &bins, int d0, int d1)
-{
-    const uint32_t kind = ma.y & 0xfu;
-    if (kind == BK_LIN4) {
-        const float4 ba = lds_v4f(bord + ma.x * 4u);
-        const float4 bb = lds_v4f(bord + mb.x * 4u);
-        const uint32_t r0 = min(ge4(x[0], ba), ma.y >> 16), r1 = min(ge4(x[1], ba), ma.y >> 16);
-        const uint32_t r2 = min(ge4(x[2], bb), mb.y >> 16), r3 = min(ge4(x[3], bb), mb.y >> 16);
-        if (SIMPLE) {
-            store_simple(bins, ma, d0, r0);
-            store_simple(bins, ma, d1, r1);
-            store_simple(bins, mb, d0, r2);
-            store_simple(bins, mb, d1, r3);
-        } else {
-            store_bin<CODES, Sink>(bins, ma, d0, r0);
-            store_bin<CODES, Sink>(bins, ma, d1, r1);
-            store_bin<CODES, Sink>(bins, mb, d0, r2);
-            store_bin<CODES, Sink>(bins, mb, d1, r3);
+#pragma unroll
+    for (int st = L - 1; st >= 0; --st) {
+        const uint32_t w = 1u << st;
+        float ea[NDL], eb[NDL];
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) {
+            ea[n] = ldsa_f32(pa[n] + 4u * skew(w - 1));
+            eb[n] = ldsa_f32(pb[n] + 4u * skew(w - 1));
         }
-        return;
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) {
+            add_if_not_less(pa[n], xa[n], ea[n], 4u * (w + (w >> 5)));
+            add_if_not_less(pb[n], xb[n], eb[n], 4u * (w + (w >> 5)));
+        }
     }
-    switch ((ma.y >> 8) & 0xffu) {
-    case 1: bin_pair<CODES, 1, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    case 2: bin_pair<CODES, 2, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    case 3: bin_pair<CODES, 3, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    case 4: bin_pair<CODES, 4, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    case 5: bin_pair<CODES, 5, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    case 6: bin_pair<CODES, 6, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    case 7: bin_pair<CODES, 7, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
-    default: bin_pair<CODES, 8, Sink, SIMPLE>(x, ma, mb, bord, bins, d0, d1); break;
+    uint32_t ra[NDL], rb[NDL];
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        ra[n] = pos_to_bin<L>(pa[n], a0, ma.y >> 16);
+        rb[n] = pos_to_bin<L>(pb[n], b0, mb.y >> 16);
     }
+    store_bins<NDL, CODES>(s, ma, d0, ra);
+    store_bins<NDL, CODES>(s, mb, d0, rb);
 }
 
-template <bool CODES, class Sink>
-__device__ __forceinline__ void pair_dispatch(const float x[4], const uint4 &ma, const uint4 &mb,
-                                              uint32_t bord, const Sink &bins, int d0, int d1)
+template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void bin_pair_dispatch(const float (&xa)[NDL], const float (&xb)[NDL],
+                                                  const uint4 &ma, const uint4 &mb, uint32_t bord,
+                                                  const Sink &s, uint32_t d0)
 {
-    if ((ma.y & 0xfu) == BK_SKIP) return;  // warp-uniform
-    // simple pair: both factors used, no second code column (set by the model compiler)
-    if (ma.y & 0x10u)
-        pair_dispatch_k<CODES, Sink, true>(x, ma, mb, bord, bins, d0, d1);
-    else
-        pair_dispatch_k<CODES, Sink, false>(x, ma, mb, bord, bins, d0, d1);
+    switch (ma.y & 0xfu) {  // warp-uniform
+    case CLS_SKIP: break;
+    case CLS_LIN4: lin4_pair<NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 2: bin_pair<1, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 3: bin_pair<2, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 4: bin_pair<3, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 5: bin_pair<4, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 6: bin_pair<5, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 7: bin_pair<6, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 8: bin_pair<7, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    default: bin_pair<8, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    }
 }
 
 // tile: the 16 KB factor box; meta: its 32 fmeta entries (512 B); bord: its
-// factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot.
-// Warp w: factor quad q = w >> 1 (two pairs) for documents 64*(w&1) + lane and
-// + 32: 4 independent search chains per lane per pair.
-template <bool CODES, class Sink>
+// factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot,
+// given as buffer offsets.  Quad q, documents d0 + 32n (n < NDL), d0 = dbase + lane.
+template <int NDL, bool CODES, class Sink>
 __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
-                                             const Sink &bins, int warp, int lane, bool fm)
+                                             const Sink &bins, int q, int dbase, int lane, bool fm)
 {
-    const int q = warp >> 1;
-    const int d0 = ((warp & 1) << 6) | lane, d1 = d0 + 32;
-    const uint4 m0 = lds_v4u(meta + 64u * q), m1 = lds_v4u(meta + 64u * q + 16u);
-    const uint4 m2 = lds_v4u(meta + 64u * q + 32u), m3 = lds_v4u(meta + 64u * q + 48u);
-    if (((m0.y | m2.y) & 0xfu) == BK_SKIP) return;  // warp-uniform: no used factor in the quad
-    float4 v0, v1;
-    if (fm) {  // feature-major box [32 factors][128 docs]: 512-byte rows, lanes = docs
-        const uint32_t r = tile + q * 4 * 512;
-        v0 = make_float4(lds_f32(r + d0 * 4), lds_f32(r + 512 + d0 * 4), lds_f32(r + 1024 + d0 * 4),
-                         lds_f32(r + 1536 + d0 * 4));
-        v1 = make_float4(lds_f32(r + d1 * 4), lds_f32(r + 512 + d1 * 4), lds_f32(r + 1024 + d1 * 4),
-                         lds_f32(r + 1536 + d1 * 4));
-    } else {   // doc-major box [128 docs][32 factors], 128B-swizzled
-        v0 = lds_v4f(tile + d0 * 128 + ((q ^ (d0 & 7)) << 4));
-        v1 = lds_v4f(tile + d1 * 128 + ((q ^ (d1 & 7)) << 4));
+    const uint32_t ma_ = sabs(meta) + 64u * q;
+    const uint4 m0 = ldsa_v4u(ma_), m2 = ldsa_v4u(ma_ + 32u);
+    if (((m0.y | m2.y) & 0xfu) == CLS_SKIP) return;  // warp-uniform: no used factor in the quad
+    const uint4 m1 = ldsa_v4u(ma_ + 16u), m3 = ldsa_v4u(ma_ + 48u);
+    const uint32_t d0 = static_cast<uint32_t>(dbase + lane);
+    const uint32_t ta = sabs(tile), ba = sabs(bord);
+    float x[4][NDL];
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        const uint32_t d = d0 + 32u * n;
+        float4 v;
+        if (fm) {  // feature-major box [32 factors][128 docs]: 512-byte rows, lanes = docs
+            const uint32_t r = ta + q * 4 * 512 + d * 4;
+            v = make_float4(ldsa_f32(r), ldsa_f32(r + 512), ldsa_f32(r + 1024), ldsa_f32(r + 1536));
+        } else {   // doc-major box [128 docs][32 factors], 128B-swizzled (d & 7 == lane & 7)
+            v = ldsa_v4f(ta + d * 128 + ((q ^ (lane & 7)) << 4));
+        }
+        x[0][n] = v.x;
+        x[1][n] = v.y;
+        x[2][n] = v.z;
+        x[3][n] = v.w;
     }
-    {
-        const float x[4] = {v0.x, v1.x, v0.y, v1.y};
-        pair_dispatch<CODES, Sink>(x, m0, m1, bord, bins, d0, d1);
-    }
-    {
-        const float x[4] = {v0.z, v1.z, v0.w, v1.w};
-        pair_dispatch<CODES, Sink>(x, m2, m3, bord, bins, d0, d1);
-    }
+    bin_pair_dispatch<NDL, CODES>(x[0], x[1], m0, m1, ba, bins, d0);
+    bin_pair_dispatch<NDL, CODES>(x[2], x[3], m2, m3, ba, bins, d0);
 }
 
 // ---------------------------------------------------------------------------
@@ -643,10 +662,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int c0 = j * p.fsub_per_job;
                 const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
                 const uint32_t sb = ring + slot * p.slot_bytes;
+#if ODF_DIAG & 1  // diagnostics build only: phase A does no work (TMA streaming rate)
+                if (nsub < 0)
+#endif
                 for (int s = 0; s < nsub; ++s)
-                    binarize_sub<MODE == MODE_FUSED, SmemSink>(
+                    binarize_sub<2, MODE == MODE_FUSED, SmemSink>(
                         sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
-                        sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp, lane, p.fm != 0);
+                        sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp >> 1,
+                        (warp & 1) << 6, lane, p.fm != 0);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty);
                 if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -670,6 +693,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
             mbar_wait(full, ph);
+#if ODF_DIAG & 2  // diagnostics build only: phase B does no work
+            if (n_bjobs < 0)
+#endif
             apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, p.desc_bytes, lane_bins, warp,
                                     p.tc / kConsumerWarps, acc);
             acc.pin(pin_scratch);
@@ -800,9 +826,8 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    binarize_sub<true, GmemSink>(t_off, m_off, b_off,
-                                 GmemSink{p.lat_codes + tile * static_cast<int64_t>(p.n_cols) * kTile},
-                                 warp, lane, p.fm != 0);
+    binarize_sub<2, true, GmemSink>(t_off, m_off, b_off, GmemSink{p.lat_codes + tile * p.code_stride},
+                                    warp >> 1, (warp & 1) << 6, lane, p.fm != 0);
 }
 
 template <int DEPTH>
@@ -818,7 +843,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const uint32_t chunk = (cols_bytes + 1023u) & ~1023u;
     const uint32_t red = chunk + ((p.chunk_bytes + 1023u) & ~1023u);
     {
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.lat_codes + tile * static_cast<int64_t>(cols_bytes));
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.lat_codes + tile * p.code_stride);
         for (uint32_t k = tid; k < cols_bytes / 16; k += kConsumerThreads) sts_v4u(bins + 16 * k, src[k]);
     }
     const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);

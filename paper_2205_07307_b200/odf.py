@@ -39,7 +39,7 @@ class _Info(ctypes.Structure):
                 ("max_borders", ctypes.c_int32), ("total_borders", ctypes.c_int64),
                 ("borders_in_smem", ctypes.c_int32), ("stages_fused", ctypes.c_int32),
                 ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32),
-                ("leaf_type", ctypes.c_int32)]
+                ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
