@@ -10,8 +10,10 @@
  *                   (true = 1; level l = bit l, least significant
  *                   first), fetch that answer and sum over trees.
  * The binarized form used here is the north_star's: per used feature f, the
- * sorted unique thresholds ("borders") b_0 < ... < b_{m-1} and the uint8 bin
- *   bin(x) = #{ j : !(x < b_j) }                        (0 <= bin <= m <= 254)
+ * sorted unique thresholds ("borders") b_0 < ... < b_{m-1} and the bin
+ *   bin(x) = #{ j : !(x < b_j) }                                 (0 <= bin <= m)
+ * stored as uint8 when every feature has m <= ODF_MAX_BORDERS (254), else as
+ * uint16 for every feature ("wide" model, m <= ODF_MAX_BORDERS_WIDE; NEXT-4)
  * for which  x < b_k  <=>  bin(x) <= k  for every border, NaN included
  * (DESIGN.md "Readings of the paper").
  *
@@ -50,18 +52,21 @@ typedef struct odf_model odf_model; /* opaque */
 typedef enum {
     ODF_OK = 0,
     ODF_E_INVALID_ARG = 1, /* a documented bound is violated (message names it) */
-    ODF_E_UNSUPPORTED = 2, /* valid but outside this build's limits (>254 borders, smem) */
+    ODF_E_UNSUPPORTED = 2, /* valid but outside this build's limits (>2032 borders, smem) */
     ODF_E_NOMEM = 3,       /* device or pinned-host allocation failed */
     ODF_E_CUDA = 4         /* CUDA runtime / launch error (message has cudaGetErrorString) */
 } odf_status;
 
 /* Bins are stored in a blocked layout: tiles of ODF_TILE_DOCS documents; tile
- * g holds n_used rows of ODF_TILE_DOCS bytes, row u = used feature u (ascending
- * raw feature id), byte j = document g*ODF_TILE_DOCS + j.  Bytes of padding
- * documents (>= n_docs) in the last tile are defined but meaningless.        */
+ * g holds n_used rows of ODF_TILE_DOCS elements, row u = used feature u
+ * (ascending raw feature id), element j = document g*ODF_TILE_DOCS + j.  An
+ * element is a uint8, or a little-endian uint16 for a wide model
+ * (odf_model_info.bins_elem_bytes).  Elements of padding documents (>= n_docs)
+ * in the last tile are defined but meaningless.                             */
 #define ODF_TILE_DOCS 128
 #define ODF_MAX_DEPTH 10
-#define ODF_MAX_BORDERS 254
+#define ODF_MAX_BORDERS 254       /* largest border count with uint8 bins */
+#define ODF_MAX_BORDERS_WIDE 2032 /* largest border count at all (uint16 bins, NEXT-4) */
 
 ODF_API int odf_version(void);                 /* ODF_VERSION_MAJOR*10000 + MINOR*100 + PATCH */
 ODF_API const char *odf_last_error(void);      /* thread-local; "" when the last call succeeded */
@@ -78,7 +83,7 @@ ODF_API const char *odf_last_error(void);      /* thread-local; "" when the last
  * The arrays are copied; the caller may free them on return.  Errors:
  *   ODF_E_INVALID_ARG  bad depth / counts / null pointer / feature index out of
  *                      range / non-finite threshold or leaf;
- *   ODF_E_UNSUPPORTED  a feature with more than ODF_MAX_BORDERS distinct
+ *   ODF_E_UNSUPPORTED  a feature with more than ODF_MAX_BORDERS_WIDE distinct
  *                      thresholds, or a model whose per-tile state exceeds the
  *                      227 KB shared-memory budget (message says which);
  *   ODF_E_NOMEM / ODF_E_CUDA.  Synchronises the device.  *out = NULL on error. */
@@ -147,12 +152,13 @@ typedef struct {
     int32_t num_sms;
     int32_t leaf_type;          /* ODF_LEAF_F32 / ODF_LEAF_U32 */
     int32_t bord_stride;        /* max bytes of one 32-factor sub-tile's border arrays */
+    int32_t bins_elem_bytes;    /* 1: uint8 bins; 2: uint16 bins (a feature has > ODF_MAX_BORDERS) */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);
 
 /* Bytes of the blocked bins buffer for n_docs documents
- * (= ceil(n_docs/ODF_TILE_DOCS) * n_used * ODF_TILE_DOCS), the number of used
+ * (= ceil(n_docs/ODF_TILE_DOCS) * n_used * ODF_TILE_DOCS * bins_elem_bytes), the number of used
  * features, and (optional, may be NULL) a library-owned pointer to their raw
  * ids, ascending, valid until odf_free_model.                                */
 ODF_API odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,

@@ -28,6 +28,7 @@ _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 _u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _i64 = ctypes.c_int64
@@ -69,7 +70,7 @@ def lib():
         L.oracle_borders.restype = _i64
         L.oracle_borders.argtypes = [_i32p, _f32p, _i64, _i32, _f32p, _i32p, _i64p]
         L.oracle_bins.restype = None
-        L.oracle_bins.argtypes = [_f32p, _i64, _i64, _i32, _f32p, _i32p, _i64p, _u8p]
+        L.oracle_bins.argtypes = [_f32p, _i64, _i64, _i32, _f32p, _i32p, _i64p, _u16p]
         L.oracle_border_index.restype = None
         L.oracle_border_index.argtypes = [_i32p, _f32p, _i64, _f32p, _i32p, _i64p, _i32p]
         L.oracle_score_u64.restype = None
@@ -180,10 +181,10 @@ def borders(feature_index, thresholds, n_features):
 
 
 def bins(x, n_features, flat, counts, offsets, n_docs=None):
-    """O4: bins for all features (unused features: 0 borders -> bin 0)."""
+    """O4: bins for all features (unused features: 0 borders -> bin 0), uint16."""
     x = _x2d(x)
     n = x.shape[0] if n_docs is None else int(n_docs)
-    out = np.zeros((n, n_features), np.uint8)
+    out = np.zeros((n, n_features), np.uint16)
     fl = _c(flat if flat.size else np.zeros(1, np.float32), np.float32)
     lib().oracle_bins(x, n, x.shape[1], int(n_features), fl, _c(counts, np.int32),
                       _c(offsets, np.int64), out)

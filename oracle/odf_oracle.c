@@ -256,10 +256,12 @@ int64_t oracle_borders(const int32_t *feature_index, const float *thresholds, in
     return total;
 }
 
-/* bin(i,f) = #{ j < m_f : !(x[i][f] < borders_f[j]) }, by a linear scan. */
+/* bin(i,f) = #{ j < m_f : !(x[i][f] < borders_f[j]) }, by a linear scan.
+ * uint16 output: the count itself, whatever m_f (the north_star's uint8 bins are
+ * the m_f <= 254 case; NEXT-4 widens them). */
 void oracle_bins(const float *x, int64_t n_docs, int64_t ld, int32_t n_features,
                  const float *borders, const int32_t *counts, const int64_t *offsets,
-                 uint8_t *bins_out /* [n_docs][n_features] */)
+                 uint16_t *bins_out /* [n_docs][n_features] */)
 {
     for (int64_t i = 0; i < n_docs; ++i)
         for (int32_t f = 0; f < n_features; ++f) {
@@ -267,7 +269,7 @@ void oracle_bins(const float *x, int64_t n_docs, int64_t ld, int32_t n_features,
             int32_t b = 0;
             for (int32_t j = 0; j < counts[f]; ++j)
                 if (!(v < borders[offsets[f] + j])) ++b;
-            bins_out[i * (int64_t)n_features + f] = (uint8_t)b;
+            bins_out[i * (int64_t)n_features + f] = (uint16_t)b;
         }
 }
 

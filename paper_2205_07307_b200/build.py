@@ -33,15 +33,30 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile_link(out: str, defines=(), verbose: bool = False) -> None:
+    """nvcc -c of every source in parallel (they are independent), then one link."""
+    from concurrent.futures import ThreadPoolExecutor
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
+              *[f"-D{d}" for d in defines]]
+    objs = [f"{out}.{os.path.splitext(src)[0]}.o" for src in SOURCES]
+
+    def cc(i):
+        subprocess.check_call([*common, "-Xptxas", "-v" if verbose else "-O3", "-c",
+                               os.path.join(CSRC, SOURCES[i]), "-o", objs[i]])
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        list(ex.map(cc, range(len(SOURCES))))
+    subprocess.check_call([nvcc(), *ARCH, "-shared", *objs, "-o", out, "-ldl"])
+    for o in objs:
+        os.remove(o)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
-           "-Xptxas", "-v" if verbose else "-O3",
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp, "-lcuda" if False else "-ldl"]
-    subprocess.check_call(cmd)
+    _compile_link(tmp, verbose=verbose)
     os.replace(tmp, LIB)
     return LIB
 
@@ -49,11 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 def build_variant(out: str, defines=()) -> str:
     """Diagnostics / A-B builds (tools only, loaded via ODF_LIB_OVERRIDE): same sources
     with extra -D flags, written to `out`.  The product library is build()'s."""
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
-           *[f"-D{d}" for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], "-o", out, "-ldl"]
     os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
-    subprocess.check_call(cmd)
+    _compile_link(out, defines)
     return out
 
 

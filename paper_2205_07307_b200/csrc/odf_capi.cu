@@ -58,13 +58,14 @@ odf_status cuda_fail(cudaError_t e, const char *what)
 }
 
 uint32_t skew_h(uint32_t p) { return p + (p >> 5); }  // as skew() in odf_kernels.cu
-constexpr uint32_t kSplitFlagH = 0x10u;                 // as kSplitFlag in odf_kernels.cu
+constexpr uint32_t kExtraShiftH = 4;  // fmeta.y bits 4-7 = code columns - 1 (as kExtraShift)
 uint32_t align_up(uint64_t v, uint64_t a) { return static_cast<uint32_t>((v + a - 1) / a * a); }
 
 struct Plan {
     uint32_t off_bins = 0, off_ring = 0, off_red = 0, off_bars = 0;
     uint32_t slot_bytes = 0, off_meta = 0, off_bord = 0;
     int stages = 0, fsub = 1;
+    uint32_t off_stage = 0;  // wide models, apply: u16 bins staging
     size_t smem = 0;
     int grid_per_sm = 1;
 };
@@ -80,6 +81,7 @@ struct odf_model {
     int64_t n_trees = 0;
     std::vector<int32_t> used_ids;
     int32_t n_used = 0, n_split = 0, n_cols = 0;
+    bool wide = false;  // some factor has > ODF_MAX_BORDERS borders: u16 bins (NEXT-4)
     int32_t max_borders = 0;
     int64_t total_borders = 0;
     int32_t n_fchunks = 0, border_floats = 0;
@@ -91,6 +93,7 @@ struct odf_model {
     float *d_borders = nullptr;
     uint8_t *d_chunks = nullptr;
     uint2 *d_splits = nullptr;
+    uint2 *d_ucols = nullptr;  // wide models: per used factor {first extra column * 128, C}
     uint2 *d_bchunk = nullptr;
     uint32_t *d_bf_base = nullptr, *d_bits_desc = nullptr;  // NEXT-3 (fp32 models)
     float *d_leaves = nullptr;
@@ -113,10 +116,15 @@ namespace {
 // ----------------------------------------------------------------------------
 bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
 {
-    // code columns + the trash column (stores of unused pair slots)
-    const uint32_t bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile, 1024);
+    // code columns + the trash column (stores of unused pair slots); the binarize
+    // kernel of a wide model stores u16 bins; the apply kernel of a wide model
+    // stages the u16 bins tile next to the code columns it expands them into
+    const uint32_t elem = (mode == MODE_BINARIZE && m.wide) ? 2u : 1u;
+    const uint32_t bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile * elem, 1024);
+    const uint32_t stage = (mode == MODE_APPLY && m.wide)
+                               ? align_up(static_cast<uint64_t>(m.n_used) * kTile * 2, 1024) : 0u;
     const uint32_t red_bytes = m.leaf_u32 ? 2 * kRedBytes : kRedBytes;
-    const uint32_t bins_region = (mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes);
+    const uint32_t bins_region = ((mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes)) + stage;
     const uint32_t bars = align_up(160 + 8u * m.n_fchunks, 128);  // barriers, scratch, bchunk copy
     // a factor sub-tile travels as [16 KB box][512 B fmeta][its border arrays]
     const uint32_t unit = kFSubBytes + kMetaBytes + m.bord_stride;
@@ -154,6 +162,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
     off += pl.stages * slot;
     pl.off_bins = off;
     pl.off_red = off;                     // reduction buffer aliases the bins (dead by then)
+    pl.off_stage = off + bins_region - stage;
     off += bins_region;
     pl.off_bars = off;
     off += bars;
@@ -206,6 +215,9 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.table_stride = m->table_stride;
     p.splits = m->d_splits;
     p.n_split = m->n_split;
+    p.wide = m->wide ? 1 : 0;
+    p.ucols = m->d_ucols;
+    p.off_stage = pl.off_stage;
     p.n_used = m->n_used;
     p.n_cols = m->n_cols;
     p.code_stride = static_cast<int64_t>(m->n_cols + 1) * kTile;
@@ -276,6 +288,7 @@ void odf_free_model(odf_model *m)
     cudaFree(m->d_borders);
     cudaFree(m->d_chunks);
     cudaFree(m->d_splits);
+    cudaFree(m->d_ucols);
     cudaFree(m->d_bchunk);
     cudaFree(m->d_bf_base);
     cudaFree(m->d_bits_desc);
@@ -456,24 +469,37 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         for (float v : b)
             if (u.empty() || !(v == u.back())) u.push_back(v);
         b.swap(u);
-        if (b.size() > ODF_MAX_BORDERS)
-            return fail(ODF_E_UNSUPPORTED, "factor %d has %zu distinct thresholds > %d (uint8 bins)",
-                        f, b.size(), ODF_MAX_BORDERS);
+        if (b.size() > ODF_MAX_BORDERS_WIDE)
+            return fail(ODF_E_UNSUPPORTED, "factor %d has %zu distinct thresholds > %d",
+                        f, b.size(), ODF_MAX_BORDERS_WIDE);
         used_of[f] = static_cast<int32_t>(m->used_ids.size());
         m->used_ids.push_back(f);
         m->max_borders = std::max<int32_t>(m->max_borders, static_cast<int32_t>(b.size()));
         m->total_borders += static_cast<int64_t>(b.size());
     }
     m->n_used = static_cast<int32_t>(m->used_ids.size());
+    // code columns: factor f with m borders has C = ceil(m / 127) 7-bit columns, the
+    // first at used_of[f], the others contiguous from colB_of[f] (after all primaries)
+    m->wide = m->max_borders > ODF_MAX_BORDERS;
+    auto n_codecols = [](size_t mm) { return static_cast<uint32_t>(std::max<size_t>(1, (mm + 126) / 127)); };
     std::vector<uint2> splits;
-    for (int32_t f : m->used_ids)
-        if (borders[f].size() > 127) {
-            colB_of[f] = m->n_used + static_cast<int32_t>(splits.size());
+    int32_t n_extra = 0;
+    for (int32_t f : m->used_ids) {
+        const uint32_t C = n_codecols(borders[f].size());
+        if (C > 1) colB_of[f] = m->n_used + n_extra;
+        if (C == 2 && !m->wide)
             splits.push_back(make_uint2(static_cast<uint32_t>(used_of[f]) * kTile,
                                         static_cast<uint32_t>(colB_of[f]) * kTile));
-        }
+        n_extra += static_cast<int32_t>(C) - 1;
+    }
     m->n_split = static_cast<int32_t>(splits.size());
-    m->n_cols = m->n_used + m->n_split;
+    m->n_cols = m->n_used + n_extra;
+    std::vector<uint2> ucols;
+    if (m->wide)
+        for (int32_t f : m->used_ids)
+            ucols.push_back(make_uint2(colB_of[f] >= 0 ? static_cast<uint32_t>(colB_of[f]) * kTile
+                                                       : static_cast<uint32_t>(m->n_cols) * kTile,
+                                       n_codecols(borders[f].size())));
 
     // ---- factor metadata + border arrays (binarize; layout in odf_internal.h) ----
     // Pairs (f, f+1), f even, share one code path: LIN4 if both have <= 4 borders,
@@ -495,7 +521,10 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         const uint32_t ma = n_borders(f), mb = n_borders(f + 1);
         if (ma == 0 && mb == 0) continue;
         const bool lin = std::max(ma, mb) <= 4;
-        const uint32_t L = lin ? 0u : ceil_log2p1(std::max(ma, mb));
+        // a factor with > 254 borders (more than two code columns) forces L >= 9, the
+        // kernel's wide search path, which stores any number of code columns
+        const uint32_t L = lin ? 0u : std::max(ceil_log2p1(std::max(ma, mb)),
+                                                std::max(ma, mb) > ODF_MAX_BORDERS ? 9u : 0u);
         const uint32_t cls = lin ? 1u : L + 1u;
         const uint32_t n_ent = lin ? 4u : (1u << L) - 1u;
         for (size_t g = f; g < f + 2; ++g) {
@@ -508,14 +537,15 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
             for (uint32_t pidx = 0; pidx < n_ent; ++pidx)
                 bflat[off + skew_h(pidx)] = pidx < npad ? -INFINITY : b[pidx - npad];
             while (bflat.size() % 4) bflat.push_back(-INFINITY);  // 16-byte aligned arrays
-            const bool split = mm > 127;
-            fmeta[g] = make_uint4(off, cls | (split ? kSplitFlagH : 0u) | (npad << 16),
+            const uint32_t extra = n_codecols(mm) - 1u;
+            fmeta[g] = make_uint4(off, cls | (extra << kExtraShiftH) | (npad << 16),
                                   static_cast<uint32_t>(used_of[g]) * kTile,
-                                  split ? static_cast<uint32_t>(colB_of[g]) * kTile : trash);
+                                  extra ? static_cast<uint32_t>(colB_of[g]) * kTile : trash);
         }
         // the unused factor of a mixed pair searches its partner's array, stores to trash
-        if (ma == 0) fmeta[f] = make_uint4(fmeta[f + 1].x, fmeta[f + 1].y & ~kSplitFlagH, trash, trash);
-        if (mb == 0) fmeta[f + 1] = make_uint4(fmeta[f].x, fmeta[f].y & ~kSplitFlagH, trash, trash);
+        const uint32_t no_extra = ~(0xfu << kExtraShiftH);
+        if (ma == 0) fmeta[f] = make_uint4(fmeta[f + 1].x, fmeta[f + 1].y & no_extra, trash, trash);
+        if (mb == 0) fmeta[f + 1] = make_uint4(fmeta[f].x, fmeta[f].y & no_extra, trash, trash);
     }
     m->border_floats = static_cast<int32_t>(bflat.size());
     // per sub-tile border ranges; fmeta.x becomes relative to its sub-tile's range
@@ -576,14 +606,11 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
             const auto &b = borders[f];
             const auto it = std::lower_bound(b.begin(), b.end(), thr, [](float a, float c) { return a < c; });
             const uint32_t k = static_cast<uint32_t>(it - b.begin());  // b[k] == thr
-            uint32_t col, K;
-            if (k + 1 <= 127) {
-                col = static_cast<uint32_t>(used_of[f]);
-                K = k + 1;
-            } else {
-                col = static_cast<uint32_t>(colB_of[f]);
-                K = k - 126;
-            }
+            // bin <= k  <=>  code of column c = k / 127 <= k - 127c
+            const uint32_t c = k / 127u;
+            const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
+                                        : static_cast<uint32_t>(colB_of[f]) + c - 1u;
+            const uint32_t K = k - 127u * c + 1u;
             desc[2 * l] = col * kTile;
             desc[2 * l + 1] = (128u - K) * 0x01010101u;
         }
@@ -635,6 +662,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         (e = up(reinterpret_cast<void **>(&m->d_borders), bflat.data(), bflat.size() * 4)) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_chunks), chunks.data(), chunks.size())) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_splits), splits.data(), splits.size() * sizeof(uint2))) != cudaSuccess ||
+        (e = up(reinterpret_cast<void **>(&m->d_ucols), ucols.data(), ucols.size() * sizeof(uint2))) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_bchunk), bchunk.data(), bchunk.size() * sizeof(uint2))) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_bf_base), bf_base.data(), bf_base.size() * 4)) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_bits_desc), bits_desc.data(), bits_desc.size() * 4)) != cudaSuccess ||
@@ -685,6 +713,7 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->num_sms = m->num_sms;
     info->leaf_type = m->leaf_u32 ? ODF_LEAF_U32 : ODF_LEAF_F32;
     info->bord_stride = static_cast<int32_t>(m->bord_stride);
+    info->bins_elem_bytes = m->wide ? 2 : 1;
     return ok();
 }
 
@@ -694,7 +723,7 @@ odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
     if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
     const int64_t tiles = (n_docs + kTile - 1) / kTile;
-    if (bytes) *bytes = static_cast<size_t>(tiles) * m->n_used * kTile;
+    if (bytes) *bytes = static_cast<size_t>(tiles) * m->n_used * kTile * (m->wide ? 2 : 1);
     if (n_used_features) *n_used_features = m->n_used;
     if (used_feature_ids) *used_feature_ids = m->used_ids.empty() ? nullptr : m->used_ids.data();
     return ok();
@@ -900,8 +929,15 @@ static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n
     const int grid = fp ? static_cast<int>(p.n_tiles)
                         : static_cast<int>((doc0 + ndoc - 1) / kTile - doc0 / kTile + 1);
     const int dstride = ((m->depth + 1) & ~1) * 8;
-    const size_t smem = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
-                        align_up(static_cast<uint64_t>(m->tc) * dstride, 16) + 1024;
+    size_t smem = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
+                  align_up(static_cast<uint64_t>(m->tc) * dstride, 1024);
+    if (m->wide) {  // u16 bins staged after the descriptors
+        p.off_stage = static_cast<uint32_t>(smem);
+        smem += align_up(static_cast<uint64_t>(m->n_used) * kTile * 2, 1024);
+    }
+    smem += 1024;
+    if (smem > static_cast<size_t>(m->max_smem))
+        return fail(ODF_E_UNSUPPORTED, "index kernel: %zu B of shared memory > %d", smem, m->max_smem);
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != m->device) cudaSetDevice(m->device);

@@ -54,8 +54,11 @@ struct KParams {
     int32_t tc;             // trees per chunk (multiple of 16)
     int64_t n_trees;
     uint32_t chunk_bytes, desc_bytes, table_stride;
-    const uint2 *splits;    // {u*128, colB*128} of factors with > 127 borders
+    const uint2 *splits;    // {u*128, colB*128} of factors with 128..254 borders (narrow models)
     int32_t n_split;
+    int32_t wide;           // 1: some factor has > 254 borders -> u16 true bins (NEXT-4)
+    const uint2 *ucols;     // wide models: [n_used] {first extra code column * 128 or trash, C}
+    uint32_t off_stage;     // wide models: shared-memory staging of a u16 bins tile
     int32_t n_used, n_cols;
     // ---- problem ----
     int64_t n_docs, n_tiles;

@@ -190,10 +190,13 @@ __device__ __forceinline__ void bulk_wait_all()
 // copies of -inf.  !(x < -inf) holds for every x (NaN included), so the count over
 // the padded array is exactly npad + bin(x): bin = count - npad, no clamping.
 // An unused factor of a pair searches its partner's array and stores into the
-// trash column; factors with > 127 borders (L = 8) also store a second code
-// column in the fused/latency paths (split flag).
+// trash column.  In the fused/latency paths a factor with m > 127 borders stores
+// C = ceil(m / 127) 7-bit code columns (fmeta.y bits 4-7 = C - 1): column c holds
+// clamp(bin - 127c, 0, 127), so a level on border k tests column k / 127 against
+// k % 127.  The binarize kernel stores true bins: u8,
+// or u16 for "wide" models (some factor with > 254 borders, NEXT-4).
 enum : uint32_t { CLS_SKIP = 0, CLS_LIN4 = 1 };  // cls >= 2: BIN with L = cls - 1
-constexpr uint32_t kSplitFlag = 0x10u;
+constexpr uint32_t kExtraShift = 4;              // fmeta.y bits 4-7: code columns - 1
 
 __host__ __device__ constexpr uint32_t skew(uint32_t p) { return p + (p >> 5); }
 
@@ -225,12 +228,22 @@ struct GmemSink {
         base[off] = static_cast<uint8_t>(v);
     }
 };
+// u16 true bins of a wide model (binarize kernel): element offsets, 2 bytes each
+struct SmemSink16 {
+    uint32_t base;
+    __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
+    {
+        sst<uint16_t>(base + 2u * off, static_cast<uint16_t>(v));
+    }
+};
 
 template <int NDL, bool CODES, class Sink>
 __device__ __forceinline__ void store_bins(const Sink &s, const uint4 &m, uint32_t d0,
                                            const uint32_t (&bin)[NDL])
 {
-    if (CODES && (m.y & kSplitFlag)) {  // warp-uniform; 7-bit code columns A and B
+    // extra code columns: 0 or 1 here (factors with > 254 borders are searched by
+    // bin_pair_wide, which stores any number of columns)
+    if (CODES && (m.y & (1u << kExtraShift))) {  // 128..254 borders: code columns A and B
 #pragma unroll
         for (int n = 0; n < NDL; ++n) {
             s.st(m.z + d0 + 32 * n, min(bin[n], 127u));
@@ -239,6 +252,22 @@ __device__ __forceinline__ void store_bins(const Sink &s, const uint4 &m, uint32
     } else {
 #pragma unroll
         for (int n = 0; n < NDL; ++n) s.st(m.z + d0 + 32 * n, bin[n]);
+    }
+}
+
+// Any number of 7-bit code columns A, B0, B1, ... (B contiguous): column c holds
+// clamp(bin - 127c, 0, 127) (wide pairs only).
+template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void store_bins_any(const Sink &s, const uint4 &m, uint32_t d0,
+                                               const uint32_t (&bin)[NDL])
+{
+    const uint32_t extra = CODES ? (m.y >> kExtraShift) & 0xfu : 0u;  // warp-uniform
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        s.st(m.z + d0 + 32 * n, extra ? min(bin[n], 127u) : bin[n]);
+#pragma unroll 1
+        for (uint32_t c = 1; c <= extra; ++c)
+            s.st(m.w + (c - 1u) * kTile + d0 + 32 * n, min(max(bin[n], 127u * c) - 127u * c, 127u));
     }
 }
 
@@ -274,7 +303,7 @@ __device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t base, uint
         return (pos - (base + 4u * npad)) >> 2;  // count >= npad always
     } else {
         uint32_t idx = (pos - base) >> 2;
-        idx -= idx / 33u;  // unskew (idx < 264)
+        idx -= idx / 33u;  // unskew: s = p + p/32 -> p = s - s/33 (exact)
         return idx - npad;
     }
 }
@@ -316,7 +345,46 @@ __device__ __forceinline__ void bin_pair(const float (&xa)[NDL], const float (&x
     store_bins<NDL, CODES>(s, mb, d0, rb);
 }
 
+// Wide factors (L = 9..11: > 254 borders or paired with such; NEXT-4): the same search with a run-time
+// step count (one compact loop instead of three unrolled copies in the I-cache).
 template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void bin_pair_wide(const float (&xa)[NDL], const float (&xb)[NDL],
+                                           const uint4 &ma, const uint4 &mb, uint32_t bord,
+                                           const Sink &s, uint32_t d0, uint32_t L)
+{
+    const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
+    uint32_t pa[NDL], pb[NDL];
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        pa[n] = a0;
+        pb[n] = b0;
+    }
+#pragma unroll 1
+    for (int st = static_cast<int>(L) - 1; st >= 0; --st) {
+        const uint32_t w = 1u << st, off = 4u * skew(w - 1), inc = 4u * (w + (w >> 5));
+        float ea[NDL], eb[NDL];
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) {
+            ea[n] = ldsa_f32(pa[n] + off);
+            eb[n] = ldsa_f32(pb[n] + off);
+        }
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) {
+            add_if_not_less(pa[n], xa[n], ea[n], inc);
+            add_if_not_less(pb[n], xb[n], eb[n], inc);
+        }
+    }
+    uint32_t ra[NDL], rb[NDL];
+#pragma unroll
+    for (int n = 0; n < NDL; ++n) {
+        ra[n] = pos_to_bin<11>(pa[n], a0, ma.y >> 16);
+        rb[n] = pos_to_bin<11>(pb[n], b0, mb.y >> 16);
+    }
+    store_bins_any<NDL, CODES>(s, ma, d0, ra);
+    store_bins_any<NDL, CODES>(s, mb, d0, rb);
+}
+
+template <int NDL, bool CODES, bool WIDE, class Sink>
 __device__ __forceinline__ void bin_pair_dispatch(const float (&xa)[NDL], const float (&xb)[NDL],
                                                   const uint4 &ma, const uint4 &mb, uint32_t bord,
                                                   const Sink &s, uint32_t d0)
@@ -331,14 +399,18 @@ __device__ __forceinline__ void bin_pair_dispatch(const float (&xa)[NDL], const 
     case 6: bin_pair<5, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
     case 7: bin_pair<6, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
     case 8: bin_pair<7, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    default: bin_pair<8, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    case 9: bin_pair<8, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
+    default:
+        if constexpr (WIDE)  // models with > 254 borders on some factor only
+            bin_pair_wide<NDL, CODES>(xa, xb, ma, mb, bord, s, d0, (ma.y & 0xfu) - 1u);
+        break;
     }
 }
 
 // tile: the 16 KB factor box; meta: its 32 fmeta entries (512 B); bord: its
 // factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot,
 // given as buffer offsets.  Quad q, documents d0 + 32n (n < NDL), d0 = dbase + lane.
-template <int NDL, bool CODES, class Sink>
+template <int NDL, bool CODES, bool WIDE, class Sink>
 __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
                                              const Sink &bins, int q, int dbase, int lane, bool fm)
 {
@@ -364,8 +436,8 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
         x[2][n] = v.z;
         x[3][n] = v.w;
     }
-    bin_pair_dispatch<NDL, CODES>(x[0], x[1], m0, m1, ba, bins, d0);
-    bin_pair_dispatch<NDL, CODES>(x[2], x[3], m2, m3, ba, bins, d0);
+    bin_pair_dispatch<NDL, CODES, WIDE>(x[0], x[1], m0, m1, ba, bins, d0);
+    bin_pair_dispatch<NDL, CODES, WIDE>(x[2], x[3], m2, m3, ba, bins, d0);
 }
 
 // ---------------------------------------------------------------------------
@@ -554,10 +626,34 @@ __device__ __forceinline__ void expand_splits(const KParams &p, uint32_t bins, i
     }
 }
 
+// Wide models (NEXT-4): u16 true bins of a tile (staged at `stage`, [n_used][128])
+// -> every code column: column A <- min(bin, 127), B_c <- clamp(bin - 127c, 0, 127)
+// (p.ucols[u] = {first B column * 128 or trash, C}).
+__device__ __forceinline__ void expand_wide(const KParams &p, uint32_t stage, uint32_t codes, int tid,
+                                            int nthr)
+{
+    for (int k = tid; k < p.n_used * (kTile / 4); k += nthr) {
+        const int u = k / (kTile / 4);
+        const uint32_t wd = (k % (kTile / 4)) * 4;  // first of the 4 documents
+        const uint2 w = sld<uint2>(stage + 2u * (u * kTile + wd));  // 4 x u16
+        const uint2 uc = p.ucols[u];
+        sts_u32(codes + u * kTile + wd,
+                prmt(__vminu2(w.x, 0x007f007fu), __vminu2(w.y, 0x007f007fu), 0x6420u));
+        for (uint32_t c = 1; c < uc.y; ++c) {
+            const uint32_t off = 127u * c * 0x00010001u;
+            sts_u32(codes + uc.x + (c - 1u) * kTile + wd,
+                    prmt(__vminu2(__vsubus2(w.x, off), 0x007f007fu),
+                         __vminu2(__vsubus2(w.y, off), 0x007f007fu), 0x6420u));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Main persistent kernel: MODE_FUSED (K3), MODE_BINARIZE (K1), MODE_APPLY (K2)
+// WIDE: model with > 254 borders on some factor (NEXT-4): the wide search path in
+// phase A, and u16 true bins from MODE_BINARIZE.
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH, bool U32>
+template <int MODE, int DEPTH, bool U32, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -578,7 +674,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_fjobs = HAS_A ? (p.n_fchunks + p.fsub_per_job - 1) / p.fsub_per_job : 0;
     const int n_bjobs = HAS_B ? p.n_tchunks : 0;
-    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile;
+    constexpr bool WIDE_BINS = MODE == MODE_BINARIZE && WIDE;
+    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile * (p.wide ? 2u : 1u);
+    const uint32_t bins_dst = (MODE == MODE_APPLY && p.wide) ? base + p.off_stage : bins;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -604,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
                     mbar_wait(bins_empty, bph ^ 1u);
                     mbar_expect_tx(bins_full, tile_bins_bytes);
-                    bulk_g2s(bins, p.bins_in + tile * tile_bins_bytes, tile_bins_bytes, bins_full);
+                    bulk_g2s(bins_dst, p.bins_in + tile * tile_bins_bytes, tile_bins_bytes, bins_full);
                     bph ^= 1u;
                 }
                 for (int j = 0; j < n_fjobs; ++j) {
@@ -666,10 +764,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (nsub < 0)
 #endif
                 for (int s = 0; s < nsub; ++s)
-                    binarize_sub<2, MODE == MODE_FUSED, SmemSink>(
-                        sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
-                        sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp >> 1,
-                        (warp & 1) << 6, lane, p.fm != 0);
+                    if constexpr (WIDE_BINS)
+                        binarize_sub<2, false, true, SmemSink16>(
+                            sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
+                            sb + p.off_bord + s * p.bord_stride, SmemSink16{bins}, warp >> 1,
+                            (warp & 1) << 6, lane, p.fm != 0);
+                    else
+                        binarize_sub<2, MODE == MODE_FUSED, WIDE, SmemSink>(
+                            sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
+                            sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp >> 1,
+                            (warp & 1) << 6, lane, p.fm != 0);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty);
                 if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -685,7 +789,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
             mbar_wait(bins_full, bph);
             bph ^= 1u;
-            expand_splits(p, bins, tid, kConsumerThreads);
+            if (p.wide)
+                expand_wide(p, base + p.off_stage, bins, tid, kConsumerThreads);
+            else
+                expand_splits(p, bins, tid, kConsumerThreads);
         }
         named_bar_consumers();  // all bins of the tile written
 
@@ -730,14 +837,18 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const uint32_t bins = base;
     const uint32_t descs = base + ((static_cast<uint32_t>(p.n_cols) * kTile + 1023u) & ~1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile;
+    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile * (p.wide ? 2u : 1u);
     const int64_t tile = (fingerprint ? 0 : p.doc0 / kTile) + blockIdx.x;
     {
+        const uint32_t dst = p.wide ? p.off_stage : bins;
         const uint4 *src = reinterpret_cast<const uint4 *>(p.bins_in + tile * tile_bins_bytes);
         for (uint32_t k = tid; k < tile_bins_bytes / 16; k += kConsumerThreads)
-            sts_v4u(bins + 16 * k, __ldg(src + k));
+            sts_v4u(dst + 16 * k, __ldg(src + k));
         __syncthreads();
-        expand_splits(p, bins, tid, kConsumerThreads);
+        if (p.wide)
+            expand_wide(p, p.off_stage, bins, tid, kConsumerThreads);
+        else
+            expand_splits(p, bins, tid, kConsumerThreads);
         __syncthreads();
     }
     const uint32_t lane_bins = bins + lane * 4u;
@@ -826,7 +937,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    binarize_sub<2, true, GmemSink>(t_off, m_off, b_off, GmemSink{p.lat_codes + tile * p.code_stride},
+    binarize_sub<2, true, true, GmemSink>(t_off, m_off, b_off, GmemSink{p.lat_codes + tile * p.code_stride},
                                     warp >> 1, (warp & 1) << 6, lane, p.fm != 0);
 }
 
@@ -894,7 +1005,8 @@ __global__ void __launch_bounds__(kConsumerThreads)
 {
     const int64_t tile = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint8_t *bt = p.bins_in + tile * static_cast<int64_t>(p.n_used) * kTile;
+    const uint8_t *bt = p.bins_in + tile * static_cast<int64_t>(p.n_used) * kTile * (p.wide ? 2 : 1);
+    const uint16_t *bt16 = reinterpret_cast<const uint16_t *>(bt);
     for (int u = warp; u < p.n_used; u += kConsumerWarps) {
         const uint32_t base = p.bf_base[u], m = p.bf_base[u + 1] - base;
 #pragma unroll 1
@@ -902,7 +1014,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
             const int64_t g = tile * (kTile / 32) + q;  // 32-document group
             if (g * 32 >= p.n_docs) break;
             const bool valid = g * 32 + lane < p.n_docs;  // padding documents: bit 0
-            const uint32_t b = valid ? bt[u * kTile + q * 32 + lane] : 0xffffffffu;
+            const uint32_t b = !valid ? 0xffffffffu
+                               : p.wide ? bt16[u * kTile + q * 32 + lane]
+                                        : bt[u * kTile + q * 32 + lane];
             uint32_t *dst = p.words + g * p.k_bin + base;
             for (uint32_t j0 = 0; j0 < m; j0 += 32) {
                 uint32_t mine = 0;
@@ -978,28 +1092,30 @@ cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cu
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH, bool U32>
+template <int MODE, int DEPTH, bool U32, bool WIDE = false>
 static const void *main_fn()
 {
-    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH, U32>);
+    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH, U32, WIDE>);
 }
 
-#define ODF_DEPTH_TABLE(M, U)                                                              \
-    {main_fn<M, 0, U>(), main_fn<M, 1, U>(), main_fn<M, 2, U>(), main_fn<M, 3, U>(),       \
-     main_fn<M, 4, U>(), main_fn<M, 5, U>(), main_fn<M, 6, U>(), main_fn<M, 7, U>(),       \
-     main_fn<M, 8, U>(), main_fn<M, 9, U>(), main_fn<M, 10, U>()}
+#define ODF_DEPTH_TABLE(M, U, W)                                                                    \
+    {main_fn<M, 0, U, W>(), main_fn<M, 1, U, W>(), main_fn<M, 2, U, W>(), main_fn<M, 3, U, W>(),     \
+     main_fn<M, 4, U, W>(), main_fn<M, 5, U, W>(), main_fn<M, 6, U, W>(), main_fn<M, 7, U, W>(),     \
+     main_fn<M, 8, U, W>(), main_fn<M, 9, U, W>(), main_fn<M, 10, U, W>()}
 
-static const void *main_kernel(int mode, int depth, bool u32 = false)
+static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide = false)
 {
-    static const void *fused[2][11] = {ODF_DEPTH_TABLE(MODE_FUSED, false),
-                                       ODF_DEPTH_TABLE(MODE_FUSED, true)};
-    static const void *apply[2][11] = {ODF_DEPTH_TABLE(MODE_APPLY, false),
-                                       ODF_DEPTH_TABLE(MODE_APPLY, true)};
-    static const void *binz = main_fn<MODE_BINARIZE, 0, false>();
+    static const void *fused[2][2][11] = {
+        {ODF_DEPTH_TABLE(MODE_FUSED, false, false), ODF_DEPTH_TABLE(MODE_FUSED, true, false)},
+        {ODF_DEPTH_TABLE(MODE_FUSED, false, true), ODF_DEPTH_TABLE(MODE_FUSED, true, true)}};
+    static const void *apply[2][11] = {ODF_DEPTH_TABLE(MODE_APPLY, false, false),
+                                       ODF_DEPTH_TABLE(MODE_APPLY, true, false)};
+    static const void *binz[2] = {main_fn<MODE_BINARIZE, 0, false, false>(),
+                                  main_fn<MODE_BINARIZE, 0, false, true>()};
     if (depth < 0 || depth > 10) return nullptr;
-    if (mode == MODE_FUSED) return fused[u32 ? 1 : 0][depth];
+    if (mode == MODE_FUSED) return fused[wide ? 1 : 0][u32 ? 1 : 0][depth];
     if (mode == MODE_APPLY) return apply[u32 ? 1 : 0][depth];
-    return binz;
+    return binz[wide ? 1 : 0];
 }
 
 template <int DEPTH>
@@ -1067,6 +1183,7 @@ cudaError_t prepare_kernels(int max_smem)
     for (int d = 0; d <= 10; ++d) {
         const void *fs[] = {main_kernel(MODE_FUSED, d), main_kernel(MODE_APPLY, d),
                             main_kernel(MODE_FUSED, d, true), main_kernel(MODE_APPLY, d, true),
+                            main_kernel(MODE_FUSED, d, false, true), main_kernel(MODE_FUSED, d, true, true),
                             index_kernel(d), lat_apply_kernel(d)};
         for (const void *f : fs) {
             cudaError_t e = opt_in(f, max_smem);
@@ -1074,6 +1191,8 @@ cudaError_t prepare_kernels(int max_smem)
         }
     }
     cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
+    if (e != cudaSuccess) return e;
+    e = opt_in(main_kernel(MODE_BINARIZE, 0, false, true), max_smem);
     if (e != cudaSuccess) return e;
     return opt_in(main_kernel(MODE_BINARIZE, 0), max_smem);
 }
@@ -1090,7 +1209,7 @@ int occupancy_main(int mode, int depth, size_t smem)
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s)
 {
-    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0);
+    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0);
     if (!f) return cudaErrorInvalidValue;
     KParams pc = p;
     CUtensorMap tm;

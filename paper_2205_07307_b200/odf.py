@@ -17,7 +17,8 @@ from . import build as _build
 
 TILE_DOCS = 128
 MAX_DEPTH = 10
-MAX_BORDERS = 254
+MAX_BORDERS = 254        # uint8 bins
+MAX_BORDERS_WIDE = 2032  # uint16 bins (wide models, NEXT-4)
 
 _STATUS = {0: "ODF_OK", 1: "ODF_E_INVALID_ARG", 2: "ODF_E_UNSUPPORTED", 3: "ODF_E_NOMEM",
            4: "ODF_E_CUDA"}
@@ -39,7 +40,8 @@ class _Info(ctypes.Structure):
                 ("max_borders", ctypes.c_int32), ("total_borders", ctypes.c_int64),
                 ("borders_in_smem", ctypes.c_int32), ("stages_fused", ctypes.c_int32),
                 ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32),
-                ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32)]
+                ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32),
+                ("bins_elem_bytes", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
@@ -155,10 +157,14 @@ def _ptr(t):
     return _vp(t.data_ptr()) if t is not None and t.numel() > 0 else _vp(0)
 
 
-def bins_to_canonical(bins: torch.Tensor, n_docs: int, n_used: int) -> torch.Tensor:
-    """Blocked layout [tile][used][128] -> [n_docs][n_used] (a view + copy, no arithmetic)."""
+def bins_to_canonical(bins: torch.Tensor, n_docs: int, n_used: int, elem_bytes: int = 1) -> torch.Tensor:
+    """Blocked layout [tile][used][128] -> [n_docs][n_used] (a view + copy, no arithmetic).
+    uint8 bins, or (elem_bytes == 2, wide models) uint16 bins returned as int32."""
     tiles = (n_docs + TILE_DOCS - 1) // TILE_DOCS
-    b = bins[: tiles * n_used * TILE_DOCS].view(tiles, n_used, TILE_DOCS)
+    b = bins[: tiles * n_used * TILE_DOCS * elem_bytes]
+    if elem_bytes == 2:
+        b = b.view(torch.int16).to(torch.int32) & 0xFFFF
+    b = b.view(tiles, n_used, TILE_DOCS)
     return b.permute(0, 2, 1).reshape(tiles * TILE_DOCS, n_used)[:n_docs]
 
 
@@ -390,4 +396,4 @@ class Model:
         return out
 
     def canonical_bins(self, bins: torch.Tensor, n_docs: int) -> torch.Tensor:
-        return bins_to_canonical(bins, n_docs, self.n_used)
+        return bins_to_canonical(bins, n_docs, self.n_used, self.info["bins_elem_bytes"])

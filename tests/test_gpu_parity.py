@@ -109,25 +109,62 @@ def test_special_values_ties_nan_zero_denormal_inf():
     full_check(case, idx_window=(0, 1000, 0, 128))
 
 
-@pytest.mark.parametrize("n_borders", [127, 128, 200, 254])
+@pytest.mark.parametrize("n_borders", [127, 128, 200, 254, 255, 381, 700, 2032])
 def test_many_borders_split_columns(n_borders):
-    # one factor carries n_borders distinct thresholds (> 127 uses two code columns)
+    # one factor carries n_borders distinct thresholds: > 127 uses C = ceil(m/127) code
+    # columns; > 254 makes the model wide (uint16 bins, NEXT-4)
     rng = np.random.default_rng(n_borders)
-    F, T, d, D = 8, 96, 6, 700
+    F, d, D = 8, 6, 700
+    T = max(96, (3 * n_borders) // (2 * d))
     pool = np.sort(rng.standard_normal(n_borders).astype(np.float32))
     fi = rng.integers(0, F, T * d).astype(np.int32)
+    fi[fi == 3] = 4  # factor 3 gets exactly the pool's n_borders thresholds
     thr = rng.standard_normal(T * d).astype(np.float32)
     first = np.arange(n_borders)
     fi[first] = 3
     thr[first] = pool
     hot = rng.random(T * d) < 0.3
+    hot[:n_borders] = False  # keep every pool value: exactly n_borders distinct borders
     fi[hot] = 3
     thr[hot] = pool[rng.integers(0, n_borders, hot.sum())]
     x = rng.standard_normal((D, F)).astype(np.float32)
     x[::3, 3] = pool[rng.integers(0, n_borders, x[::3, 3].size)]  # ties on the hot factor
     lv = rng.normal(0, 0.01, T << d).astype(np.float32)
     case = synth.ForestCase("split", x, F, fi, thr, lv, d, T)
-    full_check(case, idx_window=(0, D, 0, T))
+    f = full_check(case, idx_window=(0, D, 0, T))
+    m = cuda_model(case)
+    assert m.info["bins_elem_bytes"] == (2 if n_borders > 254 else 1)
+    xd = to_dev(case.x)
+    # the other consumers of bins / codes on the same model
+    bins = m.binarize(xd)
+    nbytes, k = m.bits_layout(D)
+    words = m.bits_from_bins(bins, D)[: nbytes // 4].cpu().numpy().view(np.uint32).reshape(-1, k)
+    per, flat, counts, offs = oracle.borders(case.feature_index, case.thresholds, case.n_features)
+    assert np.array_equal(words, oracle.condition_words(case.x, F, flat, counts, offs))
+    assert np.array_equal(m.apply_bits(m.bits_from_bins(bins, D), D).cpu().numpy().view(np.uint32),
+                          f.view(np.uint32))
+    ws = m.latency_workspace(D)
+    lat = m.score_latency(xd, ws).cpu().numpy()
+    assert np.abs(lat.astype(np.float64) - f).max() <= tolerance(case.leaf_values, d)
+    m.close()
+
+
+def test_too_many_borders_unsupported():
+    from paper_2205_07307_b200 import MAX_BORDERS_WIDE, OdfError
+    n = MAX_BORDERS_WIDE + 1
+    rng = np.random.default_rng(5)
+    d = 6
+    T = (n + d - 1) // d
+    fi = np.zeros(T * d, np.int32)
+    thr = np.zeros(T * d, np.float32)
+    thr[:n] = np.sort(rng.standard_normal(n).astype(np.float32))
+    thr[n:] = thr[0]
+    assert np.unique(thr).size == n
+    case = synth.ForestCase("toomany", np.zeros((4, 2), np.float32), 2, fi, thr,
+                            np.zeros(T << d, np.float32), d, T)
+    with pytest.raises(OdfError) as e:
+        cuda_model(case)
+    assert e.value.status == 2  # ODF_E_UNSUPPORTED
 
 
 def test_zero_docs_zero_trees_depth0():
@@ -161,16 +198,6 @@ def test_invalid_factor_layouts_rejected():
         m.score(x)  # ld = 6 is not a multiple of 4 (TMA row alignment)
     assert e.value.status == 1
     m.close()
-
-
-def test_too_many_borders_unsupported():
-    from paper_2205_07307_b200 import Model, OdfError
-    thr = np.arange(255, dtype=np.float32)
-    fi = np.zeros(255, np.int32)
-    lv = np.zeros(255 * 2, np.float32)
-    with pytest.raises(OdfError) as e:
-        Model(fi, thr, lv, 1, 1)
-    assert e.value.status == 2
 
 
 def test_score_independent_of_batch_and_offset():

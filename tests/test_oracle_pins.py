@@ -195,6 +195,26 @@ def test_bins_reproduce_every_raw_comparison(name, n_docs):
     assert np.array_equal(raw, via_bins)
 
 
+@pytest.mark.parametrize("m", [255, 700, 2032])
+def test_wide_bins_reproduce_every_raw_comparison(m):
+    # NEXT-4: more than 254 borders on one factor -> bins above 255 (uint16); the
+    # invariant x < b_k  <=>  bin <= k must hold on every border, ties included
+    rng = np.random.default_rng(m)
+    thr = np.sort(rng.standard_normal(m).astype(np.float32))
+    thr = np.unique(thr)
+    fi = np.zeros(thr.size, np.int32)
+    per, flat, counts, offs = oracle.borders(fi, thr, 1)
+    x = np.concatenate([rng.standard_normal(400).astype(np.float32), thr[::7],
+                        np.array([np.inf, -np.inf, np.nan], np.float32)]).reshape(-1, 1)
+    b = oracle.bins(x, 1, flat, counts, offs)[:, 0]
+    assert b.dtype == np.uint16 and b.max() == thr.size  # +inf / NaN count every border
+    k = oracle.border_index(fi, thr, flat, counts, offs)
+    assert np.array_equal(k, np.arange(thr.size))
+    with np.errstate(invalid="ignore"):
+        raw = x[:, 0][:, None] < thr[None, :]
+    assert np.array_equal(raw, b.astype(np.int64)[:, None] <= k[None, :])
+
+
 def test_bins_with_injected_ties_nan_zero_denormal():
     c = synth.tiny_case(seed=21, n_docs=256, n_features=8, n_trees=32, depth=4, pool=6)
     x = c.x.copy()
