@@ -538,7 +538,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
                 bflat[off + skew_h(pidx)] = pidx < npad ? -INFINITY : b[pidx - npad];
             while (bflat.size() % 4) bflat.push_back(-INFINITY);  // 16-byte aligned arrays
             const uint32_t extra = n_codecols(mm) - 1u;
-            fmeta[g] = make_uint4(off, cls | (extra << kExtraShiftH) | (npad << 16),
+            fmeta[g] = make_uint4(off, cls | (extra << kExtraShiftH) | ((0u - npad) << 16),
                                   static_cast<uint32_t>(used_of[g]) * kTile,
                                   extra ? static_cast<uint32_t>(colB_of[g]) * kTile : trash);
         }
@@ -561,7 +561,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         }
         if (hi == 0) continue;
         for (int32_t f = c * kFSub; f < (c + 1) * kFSub; ++f)
-            if ((fmeta[f].y & 0xfu) != 0) fmeta[f].x -= lo;
+            if ((fmeta[f].y & 0xfu) != 0) fmeta[f].x = (fmeta[f].x - lo) * 4u;  // bytes
         bchunk[c] = make_uint2(lo * 4u, (hi - lo) * 4u);
         m->bord_stride = std::max(m->bord_stride, (hi - lo) * 4u);
     }

@@ -37,10 +37,10 @@ enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 // Per-launch parameters (passed by value; all pointers are device pointers).
 struct KParams {
     // ---- binarization (stage 1) ----
-    const uint4 *fmeta;     // [n_fchunks*32] per raw factor: {array offset (floats, relative to
-                            //  its sub-tile's border block, 16 B aligned), cls | flags | npad<<16,
-                            //  colA*128, colB*128}; cls 0 unused, 1 LIN4, L+1 BIN(L); flag 0x10
-                            //  split (> 127 borders); unused slots of a pair: trash column
+    const uint4 *fmeta;     // [n_fchunks*32] per raw factor: {array byte offset (relative to its
+                            //  sub-tile's border block, 16 B aligned), cls | (C-1)<<4 | (-npad)<<16,
+                            //  colA*128, colB*128}; cls 0 unused, 1 LIN4, L+1 BIN(L); C code
+                            //  columns (> 127 borders); unused slots of a pair: trash column
     const float *borders;   // per used factor: npad x -inf then its m sorted borders; LIN4
                             // arrays have 4 entries, BIN(L) arrays 2^L-1 entries stored skewed
                             // (position p at p + (p >> 5))

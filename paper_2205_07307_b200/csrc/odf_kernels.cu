@@ -215,6 +215,12 @@ __device__ __forceinline__ void add_if_not_less(uint32_t &v, float x, float b, u
         : "f"(x), "f"(b), "r"(inc));
 }
 
+// fmeta.y bits 16-31 hold -npad (two's complement, 16 bits)
+__device__ __forceinline__ uint32_t neg_npad(const uint4 &m)
+{
+    return static_cast<uint32_t>(static_cast<int32_t>(m.y) >> 16);
+}
+
 // Where the bins / codes of a tile go: shared memory (fused, binarize) or a
 // global [n_cols + 1][128] block (latency path).
 struct SmemSink {
@@ -276,8 +282,8 @@ __device__ __forceinline__ void lin4_pair(const float (&xa)[NDL], const float (&
                                           const uint4 &ma, const uint4 &mb, uint32_t bord,
                                           const Sink &s, uint32_t d0)
 {
-    const float4 ea = ldsa_v4f(bord + ma.x * 4u), eb = ldsa_v4f(bord + mb.x * 4u);
-    const uint32_t na = 0u - (ma.y >> 16), nb = 0u - (mb.y >> 16);  // -npad
+    const float4 ea = ldsa_v4f(bord + ma.x), eb = ldsa_v4f(bord + mb.x);
+    const uint32_t na = neg_npad(ma), nb = neg_npad(mb);
     uint32_t ra[NDL], rb[NDL];
 #pragma unroll
     for (int n = 0; n < NDL; ++n) {
@@ -297,14 +303,14 @@ __device__ __forceinline__ void lin4_pair(const float (&xa)[NDL], const float (&
 }
 
 template <int L>
-__device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t base, uint32_t npad)
+__device__ __forceinline__ uint32_t pos_to_bin(uint32_t pos, uint32_t base, uint32_t nnpad)
 {
     if constexpr (L <= 5) {
-        return (pos - (base + 4u * npad)) >> 2;  // count >= npad always
+        return (pos - base + 4u * nnpad) >> 2;  // count >= npad always
     } else {
         uint32_t idx = (pos - base) >> 2;
         idx -= idx / 33u;  // unskew: s = p + p/32 -> p = s - s/33 (exact)
-        return idx - npad;
+        return idx + nnpad;
     }
 }
 
@@ -313,7 +319,7 @@ __device__ __forceinline__ void bin_pair(const float (&xa)[NDL], const float (&x
                                          const uint4 &ma, const uint4 &mb, uint32_t bord,
                                          const Sink &s, uint32_t d0)
 {
-    const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
+    const uint32_t a0 = bord + ma.x, b0 = bord + mb.x;
     uint32_t pa[NDL], pb[NDL];
 #pragma unroll
     for (int n = 0; n < NDL; ++n) {
@@ -338,8 +344,8 @@ __device__ __forceinline__ void bin_pair(const float (&xa)[NDL], const float (&x
     uint32_t ra[NDL], rb[NDL];
 #pragma unroll
     for (int n = 0; n < NDL; ++n) {
-        ra[n] = pos_to_bin<L>(pa[n], a0, ma.y >> 16);
-        rb[n] = pos_to_bin<L>(pb[n], b0, mb.y >> 16);
+        ra[n] = pos_to_bin<L>(pa[n], a0, neg_npad(ma));
+        rb[n] = pos_to_bin<L>(pb[n], b0, neg_npad(mb));
     }
     store_bins<NDL, CODES>(s, ma, d0, ra);
     store_bins<NDL, CODES>(s, mb, d0, rb);
@@ -352,7 +358,7 @@ __device__ __forceinline__ void bin_pair_wide(const float (&xa)[NDL], const floa
                                            const uint4 &ma, const uint4 &mb, uint32_t bord,
                                            const Sink &s, uint32_t d0, uint32_t L)
 {
-    const uint32_t a0 = bord + ma.x * 4u, b0 = bord + mb.x * 4u;
+    const uint32_t a0 = bord + ma.x, b0 = bord + mb.x;
     uint32_t pa[NDL], pb[NDL];
 #pragma unroll
     for (int n = 0; n < NDL; ++n) {
@@ -377,8 +383,8 @@ __device__ __forceinline__ void bin_pair_wide(const float (&xa)[NDL], const floa
     uint32_t ra[NDL], rb[NDL];
 #pragma unroll
     for (int n = 0; n < NDL; ++n) {
-        ra[n] = pos_to_bin<11>(pa[n], a0, ma.y >> 16);
-        rb[n] = pos_to_bin<11>(pb[n], b0, mb.y >> 16);
+        ra[n] = pos_to_bin<11>(pa[n], a0, neg_npad(ma));
+        rb[n] = pos_to_bin<11>(pb[n], b0, neg_npad(mb));
     }
     store_bins_any<NDL, CODES>(s, ma, d0, ra);
     store_bins_any<NDL, CODES>(s, mb, d0, rb);
@@ -410,9 +416,9 @@ __device__ __forceinline__ void bin_pair_dispatch(const float (&xa)[NDL], const 
 // tile: the 16 KB factor box; meta: its 32 fmeta entries (512 B); bord: its
 // factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot,
 // given as buffer offsets.  Quad q, documents d0 + 32n (n < NDL), d0 = dbase + lane.
-template <int NDL, bool CODES, bool WIDE, class Sink>
+template <int NDL, bool CODES, bool WIDE, bool FM, class Sink>
 __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
-                                             const Sink &bins, int q, int dbase, int lane, bool fm)
+                                             const Sink &bins, int q, int dbase, int lane)
 {
     const uint32_t ma_ = sabs(meta) + 64u * q;
     const uint4 m0 = ldsa_v4u(ma_), m2 = ldsa_v4u(ma_ + 32u);
@@ -425,7 +431,7 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
     for (int n = 0; n < NDL; ++n) {
         const uint32_t d = d0 + 32u * n;
         float4 v;
-        if (fm) {  // feature-major box [32 factors][128 docs]: 512-byte rows, lanes = docs
+        if constexpr (FM) {  // feature-major box [32 factors][128 docs]: 512-byte rows, lanes = docs
             const uint32_t r = ta + q * 4 * 512 + d * 4;
             v = make_float4(ldsa_f32(r), ldsa_f32(r + 512), ldsa_f32(r + 1024), ldsa_f32(r + 1536));
         } else {   // doc-major box [128 docs][32 factors], 128B-swizzled (d & 7 == lane & 7)
@@ -572,12 +578,17 @@ struct Acc<true> {
     }
 };
 
+#ifndef ODF_APPLY_UNROLL
+#define ODF_APPLY_UNROLL 2
+#endif
+constexpr int kApplyUnroll = ODF_APPLY_UNROLL;  // trees in flight per warp
+
 template <int DEPTH, bool U32>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
                                             int warp, int nk, Acc<U32> &acc)
 {
     // chunks hold nk * 16 trees (the last one padded with zero-answer trees)
-#pragma unroll 2
+#pragma unroll kApplyUnroll
     for (int k = 0; k < nk; ++k) {
         const int i = warp + k * kConsumerWarps;
         const uint32_t d = chunk + i * desc_stride(DEPTH);
@@ -644,6 +655,38 @@ __device__ __forceinline__ void expand_wide(const KParams &p, uint32_t stage, ui
             sts_u32(codes + uc.x + (c - 1u) * kTile + wd,
                     prmt(__vminu2(__vsubus2(w.x, off), 0x007f007fu),
                          __vminu2(__vsubus2(w.y, off), 0x007f007fu), 0x6420u));
+        }
+    }
+}
+
+// Phase A of one tile: the tile's factor jobs from the ring (slot / phase carried
+// across phases and tiles).  Warp w binarizes quad w >> 1 of every sub-tile for
+// documents 64 * (w & 1) + lane (+ 32).  Parameters are read once into registers.
+template <bool CODES, bool WIDE, bool FM, class Sink>
+__device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint32_t ring, uint32_t bars,
+                                        int n_fjobs, int S, int warp, int lane, uint32_t &slot,
+                                        uint32_t &ph)
+{
+    const int fsub = p.fsub_per_job, n_fchunks = p.n_fchunks;
+    const uint32_t slot_bytes = p.slot_bytes, off_meta = p.off_meta, off_bord = p.off_bord,
+                   bord_stride = p.bord_stride;
+    const int q = warp >> 1, dbase = (warp & 1) << 6;
+    for (int j = 0; j < n_fjobs; ++j) {
+        const uint32_t full = bars + 16u * slot, empty = full + 8u;
+        mbar_wait(full, ph);
+        const int nsub = min(fsub, n_fchunks - j * fsub);
+        const uint32_t sb = ring + slot * slot_bytes;
+#if ODF_DIAG & 1  // diagnostics build only: phase A does no work (TMA streaming rate)
+        if (nsub < 0)
+#endif
+        for (int s = 0; s < nsub; ++s)
+            binarize_sub<2, CODES, WIDE, FM>(sb + s * kFSubBytes, sb + off_meta + s * kMetaBytes,
+                                             sb + off_bord + s * bord_stride, sink, q, dbase, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty);
+        if (++slot == static_cast<uint32_t>(S)) {
+            slot = 0;
+            ph ^= 1u;
         }
     }
 }
@@ -754,29 +797,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_consumers();
         }
         if (HAS_A) {
-            for (int j = 0; j < n_fjobs; ++j) {
-                const uint32_t full = bars + 16u * slot, empty = full + 8u;
-                mbar_wait(full, ph);
-                const int c0 = j * p.fsub_per_job;
-                const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
-                const uint32_t sb = ring + slot * p.slot_bytes;
-#if ODF_DIAG & 1  // diagnostics build only: phase A does no work (TMA streaming rate)
-                if (nsub < 0)
-#endif
-                for (int s = 0; s < nsub; ++s)
-                    if constexpr (WIDE_BINS)
-                        binarize_sub<2, false, true, SmemSink16>(
-                            sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
-                            sb + p.off_bord + s * p.bord_stride, SmemSink16{bins}, warp >> 1,
-                            (warp & 1) << 6, lane, p.fm != 0);
-                    else
-                        binarize_sub<2, MODE == MODE_FUSED, WIDE, SmemSink>(
-                            sb + s * kFSubBytes, sb + p.off_meta + s * kMetaBytes,
-                            sb + p.off_bord + s * p.bord_stride, SmemSink{bins}, warp >> 1,
-                            (warp & 1) << 6, lane, p.fm != 0);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty);
-                if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+            if constexpr (WIDE_BINS) {
+                if (p.fm)
+                    phase_a<false, true, true>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph);
+                else
+                    phase_a<false, true, false>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph);
+            } else {
+                if (p.fm)
+                    phase_a<MODE == MODE_FUSED, WIDE, true>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp, lane,
+                                                            slot, ph);
+                else
+                    phase_a<MODE == MODE_FUSED, WIDE, false>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp,
+                                                             lane, slot, ph);
             }
         }
         if (MODE == MODE_BINARIZE) {
@@ -937,8 +969,11 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    binarize_sub<2, true, true, GmemSink>(t_off, m_off, b_off, GmemSink{p.lat_codes + tile * p.code_stride},
-                                    warp >> 1, (warp & 1) << 6, lane, p.fm != 0);
+    const GmemSink sink{p.lat_codes + tile * p.code_stride};
+    if (p.fm)
+        binarize_sub<2, true, true, true>(t_off, m_off, b_off, sink, warp >> 1, (warp & 1) << 6, lane);
+    else
+        binarize_sub<2, true, true, false>(t_off, m_off, b_off, sink, warp >> 1, (warp & 1) << 6, lane);
 }
 
 template <int DEPTH>
