@@ -34,22 +34,39 @@ def _stale() -> bool:
 
 
 def _compile_link(out: str, defines=(), verbose: bool = False) -> None:
-    """nvcc -c of every source in parallel (they are independent), then one link."""
+    """nvcc -c of every source in parallel (they are independent), then one link.
+    Objects are cached under build/obj/, keyed by the flags and the bytes of the
+    source and headers."""
+    import hashlib
     from concurrent.futures import ThreadPoolExecutor
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
               *[f"-D{d}" for d in defines]]
-    objs = [f"{out}.{os.path.splitext(src)[0]}.o" for src in SOURCES]
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    headers = sorted([os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")] +
+                     [os.path.join(ROOT, "include", "odf.h")])
+
+    def key(src):  # flags + the bytes of the source and every header it may include
+        h = hashlib.sha1(" ".join(common).encode())
+        for f in [src, *headers]:
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+        return h.hexdigest()[:16]
+
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    objs = [os.path.join(objdir, f"{os.path.splitext(s)[0]}.{key(p)}.o") for s, p in zip(SOURCES, srcs)]
 
     def cc(i):
-        subprocess.check_call([*common, "-Xptxas", "-v" if verbose else "-O3", "-c",
-                               os.path.join(CSRC, SOURCES[i]), "-o", objs[i]])
+        if os.path.exists(objs[i]) and not verbose:
+            return
+        tmp = objs[i] + f".tmp{os.getpid()}"
+        subprocess.check_call([*common, "-Xptxas", "-v" if verbose else "-O3", "-c", srcs[i], "-o", tmp])
+        os.replace(tmp, objs[i])
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         list(ex.map(cc, range(len(SOURCES))))
     subprocess.check_call([nvcc(), *ARCH, "-shared", *objs, "-o", out, "-ldl"])
-    for o in objs:
-        os.remove(o)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

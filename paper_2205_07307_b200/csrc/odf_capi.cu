@@ -21,6 +21,7 @@
 #include <memory>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -60,6 +61,13 @@ odf_status cuda_fail(cudaError_t e, const char *what)
 uint32_t skew_h(uint32_t p) { return p + (p >> 5); }  // as skew() in odf_kernels.cu
 constexpr uint32_t kExtraShiftH = 4;  // fmeta.y bits 4-7 = code columns - 1 (as kExtraShift)
 uint32_t align_up(uint64_t v, uint64_t a) { return static_cast<uint32_t>((v + a - 1) / a * a); }
+// Ring-geometry tuning knobs (diagnostics sweeps; unset = the built-in policy):
+// ODF_RING_SUBS = factor sub-tiles per fused ring slot (1 or 2), ODF_RING_STAGES_MAX.
+int env_int(const char *name, int dflt)
+{
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
 
 struct Plan {
     uint32_t off_bins = 0, off_ring = 0, off_red = 0, off_bars = 0;
@@ -137,8 +145,9 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
         slot = align_up(m.chunk_bytes, 1024);
         smax = 4;
     } else {
-        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(2u * unit, 1024));
-        smax = 8;
+        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024),
+                                  align_up((env_int("ODF_RING_SUBS", 2) == 1 ? 1u : 2u) * unit, 1024));
+        smax = env_int("ODF_RING_STAGES_MAX", 8);
     }
     const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
     const int64_t fixed = static_cast<int64_t>(bins_region) + bars;
@@ -579,7 +588,9 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
                                                2 * kRedBytes);
         const int64_t room = static_cast<int64_t>(max_smem) - 1024 - 1024 - bins;  // for >= 2 slots
         uint32_t target = 20480u;
-        if (room / 2 >= static_cast<int64_t>(align_up(2u * unit, 1024))) target = 2u * unit;
+        const int subs = env_int("ODF_RING_SUBS", 2);
+        if (subs == 1) target = unit;
+        else if (room / 2 >= static_cast<int64_t>(align_up(2u * unit, 1024))) target = 2u * unit;
         const uint32_t per = static_cast<uint32_t>(dstride) + m->table_stride;
         m->tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, target / (16u * per)));
     }

@@ -33,6 +33,20 @@
 
 namespace odf {
 
+#if ODF_DIAG & 8  // diagnostics build only: per-warp phase timeline (tools/timeline.py)
+constexpr int kDiagIt = 64;  // tile iterations recorded per CTA
+__device__ unsigned long long g_diag[148 * kDiagIt * 16 * 8];
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DIAG_T(var) const unsigned long long var = gtime()
+#else
+#define DIAG_T(var)
+#endif
+
 // ---------------------------------------------------------------------------
 // Shared memory: one dynamic buffer, addressed by byte OFFSETS from its start.
 // Plain C++ loads/stores (compiler-schedulable LDS/STS); the asynchronous
@@ -78,6 +92,12 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
 // Loads by ABSOLUTE shared-window address (stage 1: read-only TMA-slot data, so
 // volatile asm keeps them after the slot's mbarrier wait; ptxas still schedules
 // them and folds constant offsets into the LDS immediate).
+__device__ __forceinline__ uint32_t ldsa_u32(uint32_t a)
+{
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
 __device__ __forceinline__ float ldsa_f32(uint32_t a)
 {
     float r;
@@ -507,7 +527,8 @@ __device__ __forceinline__ void tree_findex(uint32_t d, uint32_t lane_bins, uint
     }
 }
 
-// Shared-memory addresses of the 4 leaves (tables reversed; table base tb).
+// Absolute shared-window addresses of the 4 leaves (tables reversed; tb = the
+// table base, absolute and 256-aligned).
 template <int DEPTH>
 __device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint32_t tb,
                                            uint32_t a[4])
@@ -539,7 +560,22 @@ struct Acc;
 template <>
 struct Acc<false> {
     float v[4] = {0.f, 0.f, 0.f, 0.f};
-    __device__ __forceinline__ void add(int n, uint32_t addr) { v[n] += lds_f32(addr); }
+    // x += a, y += b as one packed FADD2 (each lane an IEEE round-to-nearest add: the
+    // same results as two FADDs)
+    static __device__ __forceinline__ void add2(float &x, float &y, float a, float b)
+    {
+        asm("{\n\t.reg .b64 p, q;\n\tmov.b64 p, {%0, %1};\n\tmov.b64 q, {%2, %3};\n\t"
+            "add.rn.f32x2 p, p, q;\n\tmov.b64 {%0, %1}, p;\n\t}"
+            : "+f"(x), "+f"(y)
+            : "f"(a), "f"(b));
+    }
+    // leaves at ABSOLUTE shared-window addresses a[n]
+    __device__ __forceinline__ void add4(const uint32_t (&a)[4])
+    {
+        const float g0 = ldsa_f32(a[0]), g1 = ldsa_f32(a[1]), g2 = ldsa_f32(a[2]), g3 = ldsa_f32(a[3]);
+        add2(v[0], v[1], g0, g1);
+        add2(v[2], v[3], g2, g3);
+    }
     // Force the accumulators (hence every gather of the chunk) to be complete before
     // what follows, i.e. before the mbarrier arrive that hands the slot back to the
     // producer (ptxas may otherwise sink the FADDs, leaving gathers in flight).
@@ -562,7 +598,11 @@ struct Acc<false> {
 template <>
 struct Acc<true> {
     unsigned long long v[4] = {0ull, 0ull, 0ull, 0ull};
-    __device__ __forceinline__ void add(int n, uint32_t addr) { v[n] += lds_u32(addr); }
+    __device__ __forceinline__ void add4(const uint32_t (&a)[4])
+    {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) v[n] += ldsa_u32(a[n]);
+    }
     __device__ __forceinline__ void pin(uint32_t scratch) const
     {
         const uint32_t x = static_cast<uint32_t>(v[0] ^ v[1] ^ v[2] ^ v[3]);
@@ -592,11 +632,12 @@ __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes,
     for (int k = 0; k < nk; ++k) {
         const int i = warp + k * kConsumerWarps;
         const uint32_t d = chunk + i * desc_stride(DEPTH);
-        const uint32_t tb = chunk + desc_bytes + i * table_stride(DEPTH);
+        // absolute address of the table (256-aligned: the buffer is 1024-aligned), so
+        // leaf_addrs yields absolute leaf addresses with no base add
+        const uint32_t tb = sabs(chunk + desc_bytes + i * table_stride(DEPTH));
         uint32_t a[4];
         leaf_addrs<DEPTH>(d, lane_bins, tb, a);
-#pragma unroll
-        for (int n = 0; n < 4; ++n) acc.add(n, a[n]);
+        acc.add4(a);
     }
 }
 
@@ -665,7 +706,7 @@ __device__ __forceinline__ void expand_wide(const KParams &p, uint32_t stage, ui
 template <bool CODES, bool WIDE, bool FM, class Sink>
 __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint32_t ring, uint32_t bars,
                                         int n_fjobs, int S, int warp, int lane, uint32_t &slot,
-                                        uint32_t &ph)
+                                        uint32_t &ph, unsigned long long &wait_ns)
 {
     const int fsub = p.fsub_per_job, n_fchunks = p.n_fchunks;
     const uint32_t slot_bytes = p.slot_bytes, off_meta = p.off_meta, off_bord = p.off_bord,
@@ -673,7 +714,13 @@ __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint3
     const int q = warp >> 1, dbase = (warp & 1) << 6;
     for (int j = 0; j < n_fjobs; ++j) {
         const uint32_t full = bars + 16u * slot, empty = full + 8u;
+        DIAG_T(tw0);
         mbar_wait(full, ph);
+#if ODF_DIAG & 8
+        wait_ns += gtime() - tw0;
+#else
+        (void)wait_ns;
+#endif
         const int nsub = min(fsub, n_fchunks - j * fsub);
         const uint32_t sb = ring + slot * slot_bytes;
 #if ODF_DIAG & 1  // diagnostics build only: phase A does no work (TMA streaming rate)
@@ -791,7 +838,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = threadIdx.x;
     const uint32_t lane_bins = bins + lane * 4u;
     uint32_t slot = 0, ph = 0, bph = 0;
+#if ODF_DIAG & 8
+    int diag_it = 0;
+#endif
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        unsigned long long waitA = 0;
+#if ODF_DIAG & 8
+        unsigned long long waitB = 0;
+#endif
+        DIAG_T(t_start);
         if (MODE == MODE_BINARIZE && tile != blockIdx.x) {
             if (tid == 0) bulk_wait_read_all();  // previous tile's bins fully read by TMA store
             named_bar_consumers();
@@ -799,16 +854,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (HAS_A) {
             if constexpr (WIDE_BINS) {
                 if (p.fm)
-                    phase_a<false, true, true>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph);
+                    phase_a<false, true, true>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA);
                 else
-                    phase_a<false, true, false>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph);
+                    phase_a<false, true, false>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA);
             } else {
                 if (p.fm)
                     phase_a<MODE == MODE_FUSED, WIDE, true>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp, lane,
-                                                            slot, ph);
+                                                            slot, ph, waitA);
                 else
                     phase_a<MODE == MODE_FUSED, WIDE, false>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp,
-                                                             lane, slot, ph);
+                                                             lane, slot, ph, waitA);
             }
         }
         if (MODE == MODE_BINARIZE) {
@@ -826,12 +881,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
                 expand_splits(p, bins, tid, kConsumerThreads);
         }
+        DIAG_T(t_adone);
         named_bar_consumers();  // all bins of the tile written
+        DIAG_T(t_bstart);
 
         Acc<U32> acc;
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
+            DIAG_T(tw0);
             mbar_wait(full, ph);
+#if ODF_DIAG & 8
+            waitB += gtime() - tw0;
+#endif
 #if ODF_DIAG & 2  // diagnostics build only: phase B does no work
             if (n_bjobs < 0)
 #endif
@@ -842,6 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(empty);
             if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
         }
+        DIAG_T(t_bdone);
         // reduction buffer aliases the bins: wait until every warp is done with them
         named_bar_consumers();
         acc.to_red(red, warp, lane);
@@ -852,6 +914,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_consumers();
         if (MODE == MODE_APPLY && tile_bins_bytes > 0 && lane == 0) mbar_arrive(bins_empty);
+#if ODF_DIAG & 8
+        if (lane == 0 && diag_it < kDiagIt && blockIdx.x < 148) {
+            unsigned long long *d = g_diag + ((static_cast<size_t>(blockIdx.x) * kDiagIt + diag_it) * 16 + warp) * 8;
+            d[0] = t_start; d[1] = t_adone; d[2] = t_bstart; d[3] = t_bdone; d[4] = gtime();
+            d[5] = waitA; d[6] = waitB; d[7] = static_cast<unsigned long long>(tile);
+        }
+        ++diag_it;
+#endif
     }
     if (MODE == MODE_BINARIZE && tid == 0) bulk_wait_all();
 }
@@ -1268,3 +1338,18 @@ cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid
 }
 
 }  // namespace odf
+
+#if ODF_DIAG & 8
+extern "C" __attribute__((visibility("default"))) int odf_diag_copy(void *host, size_t bytes)
+{
+    if (bytes > sizeof(odf::g_diag)) bytes = sizeof(odf::g_diag);
+    return static_cast<int>(cudaMemcpyFromSymbol(host, odf::g_diag, bytes));
+}
+extern "C" __attribute__((visibility("default"))) int odf_diag_clear()
+{
+    static unsigned long long zero[1024];
+    for (size_t o = 0; o < sizeof(odf::g_diag); o += sizeof zero)
+        cudaMemcpyToSymbol(odf::g_diag, zero, sizeof zero, o);
+    return 0;
+}
+#endif
