@@ -98,6 +98,17 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _ncu_fused(cfg: str):
+    """The fused kernel's entry of the latest committed ncu capture (profiles/rN_traffic.json)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            return json.load(open(path))[cfg]["fused"], os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def _traffic(cfg: str):
     """dram read+write bytes per launch of the fused kernel from the latest committed
     ncu --set full capture (profiles/rN_traffic.json), or None."""
@@ -109,6 +120,24 @@ def _traffic(cfg: str):
         except Exception:
             continue
     return None, None
+
+
+def _binding(cfg: str, kern_ms: float, info: dict, clk) -> dict | None:
+    """The resource that binds the fused kernel (profiles/README.md):
+    shared-memory / L1 pipe wavefronts per launch from the committed ncu capture,
+    over this run's mean kernel time, against one wavefront per SM clock."""
+    ent, src = _ncu_fused(cfg)
+    if not ent or "smem_wavefronts" not in ent:
+        return None
+    mhz = clk.summary().get("sm_mhz") or clk.max_mhz
+    if not mhz:
+        return None
+    per_s = ent["smem_wavefronts"] / (kern_ms / 1000.0)
+    peak = info["num_sms"] * mhz * 1e6
+    return {"resource": "shared-memory/L1 pipe wavefronts", "achieved": per_s, "peak": peak,
+            "unit": "wavefronts/s", "frac": per_s / peak, "per_launch": ent["smem_wavefronts"],
+            "issue_active_pct_ncu": ent.get("issue_active_pct"), "source": src,
+            "peak_basis": "1 wavefront per SM per clock x SMs x SM clock during the run"}
 
 
 def _dist():
@@ -321,6 +350,7 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_kind": peak_kind, "kernel": "odf_main_kernel<FUSED,%d>" % case.depth,
                          "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes},
+            "binding": _binding(args.config, kern_ms, info, clk),
             "two_stage": {"binarize_ms": tb, "apply_ms": ta,
                           "docs_per_s": n / ((tb + ta) / 1000.0)},
             "e2e": {"value": n * k_e2e / e2e_s, "unit": "docs/s",
