@@ -1,3 +1,4 @@
+# Round-1 evidence commands (run on a gpurun box from the repo root; outputs in gpurun_out/).
 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench_c2.csv python bench.py --steps 20 --warmup 3 > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:odf_main_kernel -c 3 -o gpurun_out/prof_c2 python tools/prof_kernels.py --config c2 --iters 1 > gpurun_out/ncu_full.log 2>&1
