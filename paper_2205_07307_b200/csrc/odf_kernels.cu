@@ -415,21 +415,23 @@ __device__ __forceinline__ void bin_pair_dispatch(const float (&xa)[NDL], const 
                                                   const uint4 &ma, const uint4 &mb, uint32_t bord,
                                                   const Sink &s, uint32_t d0)
 {
-    switch (ma.y & 0xfu) {  // warp-uniform
-    case CLS_SKIP: break;
-    case CLS_LIN4: lin4_pair<NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 2: bin_pair<1, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 3: bin_pair<2, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 4: bin_pair<3, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 5: bin_pair<4, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 6: bin_pair<5, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 7: bin_pair<6, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 8: bin_pair<7, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    case 9: bin_pair<8, NDL, CODES>(xa, xb, ma, mb, bord, s, d0); break;
-    default:
-        if constexpr (WIDE)  // models with > 254 borders on some factor only
-            bin_pair_wide<NDL, CODES>(xa, xb, ma, mb, bord, s, d0, (ma.y & 0xfu) - 1u);
-        break;
+    // warp-uniform class; an if-chain ordered by frequency instead of a jump table
+    // (cls 2, 3 = BIN 1, 2 never occur: pairs with <= 4 borders are LIN4)
+    const uint32_t cls = ma.y & 0xfu;
+    if (cls == CLS_LIN4) {
+        lin4_pair<NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+    } else if (cls == CLS_SKIP) {
+    } else if (cls <= 5) {
+        if (cls == 5) bin_pair<4, NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+        else bin_pair<3, NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+    } else if (cls <= 7) {
+        if (cls == 6) bin_pair<5, NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+        else bin_pair<6, NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+    } else if (cls <= 9) {
+        if (cls == 8) bin_pair<7, NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+        else bin_pair<8, NDL, CODES>(xa, xb, ma, mb, bord, s, d0);
+    } else if constexpr (WIDE) {  // models with > 254 borders on some factor only
+        bin_pair_wide<NDL, CODES>(xa, xb, ma, mb, bord, s, d0, cls - 1u);
     }
 }
 
