@@ -555,6 +555,9 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         const uint32_t no_extra = ~(0xfu << kExtraShiftH);
         if (ma == 0) fmeta[f] = make_uint4(fmeta[f + 1].x, fmeta[f + 1].y & no_extra, trash, trash);
         if (mb == 0) fmeta[f + 1] = make_uint4(fmeta[f].x, fmeta[f].y & no_extra, trash, trash);
+        // pair flag (bit 8 of the first factor's fmeta.y): a factor of the pair has code
+        // columns beyond the first (kPairSplit in odf_kernels.cu)
+        if (((fmeta[f].y | fmeta[f + 1].y) >> kExtraShiftH) & 0xfu) fmeta[f].y |= 1u << 8;
     }
     m->border_floats = static_cast<int32_t>(bflat.size());
     // per sub-tile border ranges; fmeta.x becomes relative to its sub-tile's range

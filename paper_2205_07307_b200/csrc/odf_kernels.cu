@@ -217,6 +217,8 @@ __device__ __forceinline__ void bulk_wait_all()
 // or u16 for "wide" models (some factor with > 254 borders, NEXT-4).
 enum : uint32_t { CLS_SKIP = 0, CLS_LIN4 = 1 };  // cls >= 2: BIN with L = cls - 1
 constexpr uint32_t kExtraShift = 4;              // fmeta.y bits 4-7: code columns - 1
+constexpr uint32_t kPairSplit = 1u << 8;         // fmeta.y of a pair's first factor: a factor of
+                                                 // the pair has > 127 borders (two code columns)
 
 __host__ __device__ constexpr uint32_t skew(uint32_t p) { return p + (p >> 5); }
 
@@ -263,6 +265,11 @@ struct SmemSink16 {
     }
 };
 
+// Both factors of a pair: one warp-uniform test for code-column splits per pair.
+template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void store_pair(const Sink &s, const uint4 &ma, const uint4 &mb, uint32_t d0,
+                                           const uint32_t (&ra)[NDL], const uint32_t (&rb)[NDL]);
+
 template <int NDL, bool CODES, class Sink>
 __device__ __forceinline__ void store_bins(const Sink &s, const uint4 &m, uint32_t d0,
                                            const uint32_t (&bin)[NDL])
@@ -278,6 +285,22 @@ __device__ __forceinline__ void store_bins(const Sink &s, const uint4 &m, uint32
     } else {
 #pragma unroll
         for (int n = 0; n < NDL; ++n) s.st(m.z + d0 + 32 * n, bin[n]);
+    }
+}
+
+template <int NDL, bool CODES, class Sink>
+__device__ __forceinline__ void store_pair(const Sink &s, const uint4 &ma, const uint4 &mb, uint32_t d0,
+                                           const uint32_t (&ra)[NDL], const uint32_t (&rb)[NDL])
+{
+    if (CODES && (ma.y & kPairSplit)) {
+        store_bins<NDL, CODES>(s, ma, d0, ra);
+        store_bins<NDL, CODES>(s, mb, d0, rb);
+    } else {
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) {
+            s.st(ma.z + d0 + 32 * n, ra[n]);
+            s.st(mb.z + d0 + 32 * n, rb[n]);
+        }
     }
 }
 
@@ -318,8 +341,7 @@ __device__ __forceinline__ void lin4_pair(const float (&xa)[NDL], const float (&
         add_if_not_less(ra[n], xa[n], ea.w, 1u);
         add_if_not_less(rb[n], xb[n], eb.w, 1u);
     }
-    store_bins<NDL, CODES>(s, ma, d0, ra);
-    store_bins<NDL, CODES>(s, mb, d0, rb);
+    store_pair<NDL, CODES>(s, ma, mb, d0, ra, rb);
 }
 
 template <int L>
@@ -367,8 +389,7 @@ __device__ __forceinline__ void bin_pair(const float (&xa)[NDL], const float (&x
         ra[n] = pos_to_bin<L>(pa[n], a0, neg_npad(ma));
         rb[n] = pos_to_bin<L>(pb[n], b0, neg_npad(mb));
     }
-    store_bins<NDL, CODES>(s, ma, d0, ra);
-    store_bins<NDL, CODES>(s, mb, d0, rb);
+    store_pair<NDL, CODES>(s, ma, mb, d0, ra, rb);
 }
 
 // Wide factors (L = 9..11: > 254 borders or paired with such; NEXT-4): the same search with a run-time
