@@ -146,7 +146,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
         smax = 4;
     } else {
         slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024),
-                                  align_up((env_int("ODF_RING_SUBS", 2) == 1 ? 1u : 2u) * unit, 1024));
+                                  align_up((env_int("ODF_RING_SUBS", 1) == 1 ? 1u : 2u) * unit, 1024));
         smax = env_int("ODF_RING_STAGES_MAX", 8);
     }
     const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
@@ -581,8 +581,10 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     // ---- tree chunks: descriptors + reversed leaf tables ----
     const int dstride = desc_stride(depth);
     m->table_stride = static_cast<uint32_t>(table_stride(depth));
-    // chunk size: ~20 KB, or about two factor sub-tiles (16.5 KB + borders each) so
-    // a ring slot carries 2 sub-tiles in phase A and >= 64 trees in phase B
+    // chunk size: about one factor sub-tile (16.5 KB + its borders), so one ring slot
+    // carries a sub-tile in phase A or a chunk of similar bytes in phase B and the
+    // ring is as deep as shared memory allows (up to 8 stages: more factor data in
+    // flight while phase A runs); ODF_RING_SUBS=2 selects two-sub-tile slots
     {
         int max_smem = 0;
         cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -591,7 +593,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
                                                2 * kRedBytes);
         const int64_t room = static_cast<int64_t>(max_smem) - 1024 - 1024 - bins;  // for >= 2 slots
         uint32_t target = 20480u;
-        const int subs = env_int("ODF_RING_SUBS", 2);
+        const int subs = env_int("ODF_RING_SUBS", 1);
         if (subs == 1) target = unit;
         else if (room / 2 >= static_cast<int64_t>(align_up(2u * unit, 1024))) target = 2u * unit;
         const uint32_t per = static_cast<uint32_t>(dstride) + m->table_stride;
