@@ -361,7 +361,7 @@ def run_ours(args):
                                            "borders_in_smem", "stages_fused", "smem_fused",
                                            "total_borders", "max_borders")},
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and ws == 1:  # the oracle baseline: rank 0 at N=1 only
             line["cpu_baseline"] = cpu_baseline(case, target_s=args.ref_seconds)
         print(json.dumps(line), flush=True)
     model.close()
