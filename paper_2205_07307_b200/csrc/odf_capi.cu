@@ -11,7 +11,7 @@
 //  * 7-bit code columns: column A of f holds min(bin,127); factors with
 //    m_f > 127 also get column B = max(bin-127, 0); a node tests
 //    "code >= K" on column A with K = k+1 when k+1 <= 127, else on column B
-//    with K = k-126;  descriptor = {col*128, (128-K)*0x01010101};
+//    with K = k-126;  level descriptor = (col << 19) | (128-K)  (odf_internal.h);
 //  * leaf tables reversed (table[F] = leaf[2^d-1-F]) because the kernels
 //    assemble the complemented index F (flags are "condition false");
 //  * trees grouped in chunks of tc (multiple of 16) = [descriptors | tables].
@@ -503,6 +503,8 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     }
     m->n_split = static_cast<int32_t>(splits.size());
     m->n_cols = m->n_used + n_extra;
+    if (m->n_cols > kMaxDescCol)  // 13-bit column field of the level descriptor
+        return fail(ODF_E_UNSUPPORTED, "%d code columns > %d", m->n_cols, kMaxDescCol);
     std::vector<uint2> ucols;
     if (m->wide)
         for (int32_t f : m->used_ids)
@@ -627,8 +629,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
             const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
                                         : static_cast<uint32_t>(colB_of[f]) + c - 1u;
             const uint32_t K = k - 127u * c + 1u;
-            desc[2 * l] = col * kTile;
-            desc[2 * l + 1] = (128u - K) * 0x01010101u;
+            desc[l] = (col << 19) | (128u - K);
         }
         float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
         if (u32) {
@@ -944,7 +945,7 @@ static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n
     p.fp_out = d_fp;
     const int grid = fp ? static_cast<int>(p.n_tiles)
                         : static_cast<int>((doc0 + ndoc - 1) / kTile - doc0 / kTile + 1);
-    const int dstride = ((m->depth + 1) & ~1) * 8;
+    const int dstride = desc_stride(m->depth);
     size_t smem = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
                   align_up(static_cast<uint64_t>(m->tc) * dstride, 1024);
     if (m->wide) {  // u16 bins staged after the descriptors

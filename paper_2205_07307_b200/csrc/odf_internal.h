@@ -18,12 +18,15 @@ constexpr uint32_t kRedBytes = kConsumerWarps * kTile * 4;
 constexpr uint32_t kNoCol = 0xFFFFFFFFu;
 
 // Tree-chunk geometry, shared by the model compiler and the kernels: per tree the
-// level descriptors (8 B each, padded to an even count) and the reversed leaf table
+// level descriptors (4 B each, padded to a multiple of 4) and the reversed leaf table
 // (256 B for depth <= 6 so the PRMT address trick applies, else 4 B * 2^depth);
 // trees per chunk = a multiple of 16 (one tree per consumer warp per round) sized
 // for ~20 KB chunks.  The last chunk is padded with zero-answer trees (-0.0 / 0),
 // so the apply loop has a fixed trip count.
-__host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 1) & ~1) * 8; }
+// Level descriptor (u32): bits 19-31 = code column (col * 128 = desc >> 12), bits 0-7 =
+// 128 - K; a tree's descriptors are padded to a multiple of 4 levels (LDS.128 groups).
+constexpr int kMaxDescCol = 8191;
+__host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 3) & ~3) * 4; }
 __host__ __device__ constexpr int table_stride(int depth) { return depth <= 6 ? 256 : (4 << depth); }
 __host__ __device__ constexpr int trees_per_chunk(int depth)
 {

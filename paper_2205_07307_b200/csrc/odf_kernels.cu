@@ -494,18 +494,20 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
 // ---------------------------------------------------------------------------
 // Lane j holds documents 4j..4j+3 of the tile as the 4 bytes of one u32 read
 // from the bins row of a column.  Codes are 7-bit (factors with > 127 borders
-// use two columns), so for a level with descriptor
-// {col*128, (128-K)*0x01010101} the byte sum code + 128 - K never carries out
+// use two columns), so for a level with descriptor (col, 128-K) the
+// byte sum code + (128 - K) (the byte replicated by one PRMT) never carries out
 // of its byte and its bit 7 is the "flag" code >= K, i.e. the condition is
 // FALSE.  Flags are shifted in from the top of each byte, so after DEPTH levels
 // level l sits at bit 8-DEPTH+l: the byte is the complemented leaf index F,
 // and leaf tables are stored reversed (table[F] = leaf[2^d-1-F]).
+// Descriptors are 4 bytes per level (odf_internal.h): 6 levels cost one LDS.128
+// and one LDS.64 broadcast instead of three LDS.128.
 template <int DEPTH>
-__device__ __forceinline__ void tree_level(uint32_t col, uint32_t add, uint32_t lane_bins, int l,
-                                           uint32_t &lo, uint32_t &hi)
+__device__ __forceinline__ void tree_level(uint32_t dsc, uint32_t lane_bins, int l, uint32_t &lo,
+                                           uint32_t &hi)
 {
-    const uint32_t w = lds_u32(col + lane_bins);
-    const uint32_t s = (w + add) & 0x80808080u;
+    const uint32_t w = lds_u32(lane_bins + (dsc >> 12));  // col * 128
+    const uint32_t s = (w + prmt(dsc, 0u, 0x0000u)) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
     else
@@ -519,14 +521,19 @@ __device__ __forceinline__ void tree_flags(uint32_t d, uint32_t lane_bins, uint3
     lo = 0;
     hi = 0;
 #pragma unroll
-    for (int l = 0; l < DEPTH; l += 2) {
-        if (l + 1 < DEPTH) {
-            const uint4 q = lds_v4u(d + l * 8);
-            tree_level<DEPTH>(q.x, q.y, lane_bins, l, lo, hi);
-            tree_level<DEPTH>(q.z, q.w, lane_bins, l + 1, lo, hi);
+    for (int l = 0; l < DEPTH; l += 4) {
+        if (l + 2 < DEPTH) {  // 3 or 4 levels left: one LDS.128 (padding levels unused)
+            const uint4 q = lds_v4u(d + l * 4);
+            tree_level<DEPTH>(q.x, lane_bins, l, lo, hi);
+            tree_level<DEPTH>(q.y, lane_bins, l + 1, lo, hi);
+            tree_level<DEPTH>(q.z, lane_bins, l + 2, lo, hi);
+            if (l + 3 < DEPTH) tree_level<DEPTH>(q.w, lane_bins, l + 3, lo, hi);
+        } else if (l + 1 < DEPTH) {
+            const uint2 q = lds_v2u(d + l * 4);
+            tree_level<DEPTH>(q.x, lane_bins, l, lo, hi);
+            tree_level<DEPTH>(q.y, lane_bins, l + 1, lo, hi);
         } else {
-            const uint2 q = lds_v2u(d + l * 8);
-            tree_level<DEPTH>(q.x, q.y, lane_bins, l, lo, hi);
+            tree_level<DEPTH>(lds_u32(d + l * 4), lane_bins, l, lo, hi);
         }
     }
 }
