@@ -123,9 +123,10 @@ def _traffic(cfg: str):
 
 
 def _binding(cfg: str, kern_ms: float, info: dict, clk) -> dict | None:
-    """The resource that binds the fused kernel (profiles/README.md):
+    """The resources that bind the fused kernel (profiles/README.md):
     shared-memory / L1 pipe wavefronts per launch from the committed ncu capture,
-    over this run's mean kernel time, against one wavefront per SM clock."""
+    over this run's mean kernel time, against one wavefront per SM clock; and the
+    capture's instruction-issue utilisation.  `resource` names the busier one."""
     ent, src = _ncu_fused(cfg)
     if not ent or "smem_wavefronts" not in ent:
         return None
@@ -134,10 +135,14 @@ def _binding(cfg: str, kern_ms: float, info: dict, clk) -> dict | None:
         return None
     per_s = ent["smem_wavefronts"] / (kern_ms / 1000.0)
     peak = info["num_sms"] * mhz * 1e6
-    return {"resource": "shared-memory/L1 pipe wavefronts", "achieved": per_s, "peak": peak,
-            "unit": "wavefronts/s", "frac": per_s / peak, "per_launch": ent["smem_wavefronts"],
-            "issue_active_pct_ncu": ent.get("issue_active_pct"), "source": src,
-            "peak_basis": "1 wavefront per SM per clock x SMs x SM clock during the run"}
+    smem_frac = per_s / peak
+    issue_frac = (ent.get("issue_active_pct") or 0.0) / 100.0
+    return {"resource": "instruction issue" if issue_frac > smem_frac else "shared-memory/L1 pipe wavefronts",
+            "smem": {"achieved": per_s, "peak": peak, "unit": "wavefronts/s", "frac": smem_frac,
+                     "per_launch": ent["smem_wavefronts"],
+                     "peak_basis": "1 wavefront per SM per clock x SMs x SM clock during the run"},
+            "issue": {"frac": issue_frac, "basis": "ncu smsp__issue_active (fraction of active cycles)"},
+            "source": src}
 
 
 def _dist():
