@@ -506,7 +506,7 @@ template <int DEPTH>
 __device__ __forceinline__ void tree_level(uint32_t dsc, uint32_t lane_bins, int l, uint32_t &lo,
                                            uint32_t &hi)
 {
-    const uint32_t w = lds_u32(lane_bins + (dsc >> 12));  // col * 128
+    const uint32_t w = ldsa_u32(lane_bins + (dsc >> 12));  // col * 128; absolute address
     const uint32_t s = (w + prmt(dsc, 0u, 0x0000u)) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ========================= consumer warps =========================
     const int tid = threadIdx.x;
-    const uint32_t lane_bins = bins + lane * 4u;
+    const uint32_t lane_bins = sabs(bins) + lane * 4u;  // absolute (tree_level)
     uint32_t slot = 0, ph = 0, bph = 0;
 #if ODF_DIAG & 8
     int diag_it = 0;
@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             expand_splits(p, bins, tid, kConsumerThreads);
         __syncthreads();
     }
-    const uint32_t lane_bins = bins + lane * 4u;
+    const uint32_t lane_bins = sabs(bins) + lane * 4u;  // absolute (tree_level)
     const int64_t t_lo = fingerprint ? 0 : p.tree0;
     const int64_t t_hi = fingerprint ? p.n_trees : p.tree0 + p.ntree;
     uint64_t h[4] = {0xcbf29ce484222325ull, 0xcbf29ce484222325ull, 0xcbf29ce484222325ull,
@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
     const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
     Acc<false> acc;
-    const uint32_t lane_bins = bins + lane * 4u;
+    const uint32_t lane_bins = sabs(bins) + lane * 4u;  // absolute (tree_level)
     for (int c = c_lo; c < c_hi; ++c) {
         __syncthreads();  // previous chunk consumed (and, first time, codes stored)
         const uint4 *src = reinterpret_cast<const uint4 *>(p.chunks + static_cast<size_t>(c) * p.chunk_bytes);
