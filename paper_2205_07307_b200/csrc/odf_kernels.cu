@@ -654,20 +654,30 @@ struct Acc<true> {
 constexpr int kApplyUnroll = ODF_APPLY_UNROLL;  // trees in flight per warp
 
 template <int DEPTH, bool U32>
+__device__ __forceinline__ void apply_tree(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
+                                           int i, Acc<U32> &acc)
+{
+    const uint32_t d = chunk + i * desc_stride(DEPTH);
+    // absolute address of the table (256-aligned: the buffer is 1024-aligned), so
+    // leaf_addrs yields absolute leaf addresses with no base add
+    const uint32_t tb = sabs(chunk + desc_bytes + i * table_stride(DEPTH));
+    uint32_t a[4];
+    leaf_addrs<DEPTH>(d, lane_bins, tb, a);
+    acc.add4(a);
+}
+
+template <int DEPTH, bool U32>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
                                             int warp, int nk, Acc<U32> &acc)
 {
-    // chunks hold nk * 16 trees (the last one padded with zero-answer trees)
+    // chunks hold nk * 16 trees (the last one padded with zero-answer trees); a
+    // multiple of 4 trees per warp runs 4 trees per iteration (warp-uniform choice)
+    if (DEPTH <= 6 && (nk & 3) == 0) {
+#pragma unroll 4
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, lane_bins, warp + k * kConsumerWarps, acc);
+    } else {
 #pragma unroll kApplyUnroll
-    for (int k = 0; k < nk; ++k) {
-        const int i = warp + k * kConsumerWarps;
-        const uint32_t d = chunk + i * desc_stride(DEPTH);
-        // absolute address of the table (256-aligned: the buffer is 1024-aligned), so
-        // leaf_addrs yields absolute leaf addresses with no base add
-        const uint32_t tb = sabs(chunk + desc_bytes + i * table_stride(DEPTH));
-        uint32_t a[4];
-        leaf_addrs<DEPTH>(d, lane_bins, tb, a);
-        acc.add4(a);
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, lane_bins, warp + k * kConsumerWarps, acc);
     }
 }
 
