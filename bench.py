@@ -1,25 +1,35 @@
 #!/usr/bin/env python
 """Benchmark of the oblivious-forest hot path (binarize + apply) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--shard docs|trees]
+                    [--impl ours|reference] [--secondary c2|none]
 
-One "step" = one pass of the whole hot path (fused odf_score: binarization +
-leaf-index assembly + leaf gather/sum) over one synthetic batch of the
-workload (BASELINE.json configs[1] = c2 by default: 100,000 docs x 1,000
-factors, 2,000 depth-6 trees).  Inputs are resident in HBM when the timed
-region starts and are larger than L2 (400 MB vs 126 MB), so no L2 flush is
-needed between steps.  N > 1 (torchrun, one rank per GPU, NCCL): every rank
-scores its own batch (document sharding, weak scaling, no data-path
-collective); time = max over ranks of the CUDA-event time.
+One "step" = one pass of the whole hot path (the fused odf_score kernel:
+binarization + leaf-index assembly + leaf gather/sum) over one
+synthetic batch.  The headline workload is BASELINE.json configs[2] = c3, the
+1,000,000-document config the north_star's HBM target names (1,000,000 docs x
+1,000 factors, 10,000 depth-6 trees); c2 (configs[1]) is reported alongside in
+the same run as a secondary object.  Inputs are resident in HBM when the timed
+region starts and larger than L2 (4 GB vs 126 MB), so no L2 flush is needed.
 
-Prints ONE JSON line on rank 0 (see DESIGN.md "Measurement").
+N > 1 (torchrun, one rank per GPU, NCCL):
+  --shard docs (default): strong scaling of ONE batch: rank r scores documents
+      [floor(r*D/N), floor((r+1)*D/N)) with the replicated model and the step
+      includes the NCCL all-gather of the scores; rank 0 checks (untimed) that
+      the gathered scores are bit-identical to one GPU scoring the whole batch.
+  --shard trees (default config c4): rank r holds trees [floor(r*T/N), ...),
+      scores every document and the step includes one NCCL reduce (sum) of the
+      fp32 partial scores to rank 0; rank 0 checks the tolerance.
+time = max over ranks of the CUDA-event time of the K steps.
+
+Prints ONE JSON line on rank 0 (DESIGN.md "Measurement").
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -30,15 +40,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "documents/sec (and doc·trees/sec) for binarize+apply; % of HBM roofline"
+SMEM_BYTES_PER_CLK = 128  # shared-memory data path per SM per clock (B200_PROFILING / B300_MICROARCH)
 
 
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -98,50 +109,49 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def _ncu_fused(cfg: str):
-    """The fused kernel's entry of the latest committed ncu capture (profiles/rN_traffic.json)."""
-    import glob
+def _capture(cfg: str, kernel: str = "fused"):
+    """This kernel's counters from the latest committed ncu --set full capture
+    (profiles/rN_traffic.json, written by tools/ncu_metrics.py), or (None, None)."""
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
         try:
-            return json.load(open(path))[cfg]["fused"], os.path.relpath(path, ROOT)
+            return json.load(open(path))[cfg][kernel], os.path.relpath(path, ROOT)
         except Exception:
             continue
     return None, None
 
 
-def _traffic(cfg: str):
-    """dram read+write bytes per launch of the fused kernel from the latest committed
-    ncu --set full capture (profiles/rN_traffic.json), or None."""
-    import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
-        try:
-            return (int(json.load(open(path))[cfg]["fused"]["dram_bytes_per_launch"]),
-                    os.path.relpath(path, ROOT))
-        except Exception:
-            continue
-    return None, None
+def _roofline_hbm(n_docs, n_used, kern_ms, cfg):
+    """the fused path moves 4*F_used + 4 algorithmic bytes per document."""
+    peak, peak_kind = _peaks()
+    alg = n_docs * (4 * n_used + 4)
+    achieved = alg / (kern_ms / 1000.0) / 1e9
+    cap, src = _capture(cfg)
+    traffic = cap.get("dram_bytes_per_launch") if cap else None
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": src,
+            "peak_kind": peak_kind, "kernel": "odf_main_kernel<FUSED>", "kernel_ms": kern_ms,
+            "alg_bytes_per_launch": alg, "alg_bytes_per_doc": 4 * n_used + 4}
 
 
-def _binding(cfg: str, kern_ms: float, info: dict, clk) -> dict | None:
-    """The resources that bind the fused kernel (profiles/README.md):
-    shared-memory / L1 pipe wavefronts per launch from the committed ncu capture,
-    over this run's mean kernel time, against one wavefront per SM clock; and the
-    capture's instruction-issue utilisation.  `resource` names the busier one."""
-    ent, src = _ncu_fused(cfg)
-    if not ent or "smem_wavefronts" not in ent:
+def _roofline_smem(cfg, kern_ms, num_sms, mhz):
+    """The resource that binds the fused kernel: the SM's shared-memory
+    data path, 128 B per SM per clock.  Bytes per launch = (shared-memory load + store
+    wavefronts) x 128 B + the TMA bytes that fill shared memory (l1tex xbar->L1 read
+    bytes), from the committed ncu capture of the same build, over this run's kernel time;
+    peak = SMs x 128 B x the SM clock sampled during the run."""
+    cap, src = _capture(cfg)
+    if not cap or not mhz or "smem_ld_wavefronts" not in cap:
         return None
-    mhz = clk.summary().get("sm_mhz") or clk.max_mhz
-    if not mhz:
-        return None
-    per_s = ent["smem_wavefronts"] / (kern_ms / 1000.0)
-    peak = info["num_sms"] * mhz * 1e6
-    smem_frac = per_s / peak
-    issue_frac = (ent.get("issue_active_pct") or 0.0) / 100.0
-    return {"resource": "instruction issue" if issue_frac > smem_frac else "shared-memory/L1 pipe wavefronts",
-            "smem": {"achieved": per_s, "peak": peak, "unit": "wavefronts/s", "frac": smem_frac,
-                     "per_launch": ent["smem_wavefronts"],
-                     "peak_basis": "1 wavefront per SM per clock x SMs x SM clock during the run"},
-            "issue": {"frac": issue_frac, "basis": "ncu smsp__issue_active (fraction of active cycles)"},
+    wf = cap["smem_ld_wavefronts"] + cap.get("smem_st_wavefronts", 0.0)
+    tma = cap.get("xbar2l1tex_bytes", 0.0)
+    per_launch = wf * SMEM_BYTES_PER_CLK + tma
+    achieved = per_launch / (kern_ms / 1000.0) / 1e9
+    peak = num_sms * SMEM_BYTES_PER_CLK * mhz * 1e6 / 1e9
+    return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "bytes_per_launch": per_launch,
+            "wavefronts_per_launch": wf, "tma_bytes_per_launch": tma,
+            "issue_active": (cap.get("issue_active_pct") or 0.0) / 100.0,
+            "peak_basis": f"{num_sms} SMs x 128 B/clk x {mhz:.0f} MHz (run median)",
             "source": src}
 
 
@@ -152,15 +162,17 @@ def _dist():
     return ws, rank, local
 
 
-def _workload(cfg: str, rank: int):
+def _config(cfg: str, case, ws: int, shard: str, n_docs_total: int) -> dict:
+    """The workload description (identical for the reference arm and ours)."""
     import synth
-    from synth import CONFIGS
-    base = CONFIGS[cfg]
-    # the model is the config's; rank r scores its own batch (seed offset = rank)
-    case = synth.make_case(cfg)
-    if rank > 0:
-        case.x = synth.ranking_factors(base["seed"] + 7919 * rank, case.n_docs, case.n_features)
-    return case
+    used = int(np.unique(case.feature_index).size) if case.feature_index.size else 0
+    return {"workload": synth.WORKLOAD_NAMES[cfg], "n_docs": int(n_docs_total),
+            "n_features": int(case.n_features), "n_trees": int(case.n_trees),
+            "depth": int(case.depth), "used_features": used,
+            "l2": "inputs larger than L2 (%.0f MB > 126 MB); no flush"
+                  % (n_docs_total * case.x.shape[1] * 4 / 1e6),
+            "parallelism": ("1 GPU" if ws == 1 else f"tree-shard x{ws} + NCCL reduce"
+                            if shard == "trees" else f"doc-shard x{ws} + NCCL all-gather")}
 
 
 def cpu_baseline(case, target_s: float = 10.0):
@@ -190,36 +202,100 @@ def cpu_baseline(case, target_s: float = 10.0):
 
 
 def run_reference(args):
+    """The reference arm: the oracle (tier framing: no reference code exists), timed on
+    the host cores, each step a bounded sample of the same workload."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
     import synth
-    case = _workload(args.config, 0)
+    n_docs = synth.CONFIGS[args.config]["n_docs"]
+    case = synth.make_case(args.config, rows=(0, min(n_docs, 65536)) if args.config != "c1" else None)
     times = []
     base = None
-    # each step is a bounded sample; the whole W+K run stays within ~2 minutes
     per_step = max(0.25, min(args.ref_seconds, 120.0 / (args.warmup + args.steps)))
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
         cb = cpu_baseline(case, target_s=per_step)
-        dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(cb["value"])
             base = cb
     v = float(np.median(times))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "docs/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v * case.n_docs,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": synth.WORKLOAD_NAMES[args.config], "n_docs": case.n_docs,
-                       "n_features": case.n_features, "n_trees": case.n_trees,
-                       "depth": case.depth, "parallelism": "host threads"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v * n_docs,
+            "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(args.config, case, ws, args.shard, n_docs),
+            "doc_trees_per_s": v * case.n_trees,
             "cpu_baseline": {"value": v, "unit": "docs/s", "cores": base["cores"],
                              "kind": "oracle", "sample": base["sample"]},
             "e2e": {"value": v, "unit": "docs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _time_steps(step, steps, stream, ws, dev, clk=None):
+    """K timed steps bracketed by barrier + synchronize, CUDA events on `stream`;
+    returns (max over ranks of the total ms, this rank's mean per-step ms)."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    ctx = clk if clk is not None else _Null()
+    with ctx:
+        t0.record(stream)
+        for i in range(steps):
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    per = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    return total_ms, per
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def _secondary(cfg, steps, warmup, dev, stream):
+    """A second workload (default c2) on one GPU in the same run: fused odf_score time,
+    docs/s and HBM roofline fraction (no cpu_baseline / e2e)."""
+    import torch
+    import synth
+    from paper_2205_07307_b200 import Model
+    case = synth.make_case(cfg)
+    m = Model(case.feature_index, case.thresholds, case.leaf_values, case.depth,
+              case.n_features, device=dev.index)
+    x = torch.from_numpy(case.x).to(dev)
+    out = torch.empty(case.n_docs, dtype=torch.float32, device=dev)
+    for _ in range(warmup):
+        m.score(x, out=out, stream=stream)
+    total_ms, kern_ms = _time_steps(lambda: m.score(x, out=out, stream=stream), steps, stream, 1, dev)
+    n_used = m.info["n_used_features"]
+    res = {"workload": synth.WORKLOAD_NAMES[cfg], "value": case.n_docs * steps / (total_ms / 1e3),
+           "unit": "docs/s", "ms_per_step": total_ms / steps, "steps": steps,
+           "doc_trees_per_s": case.n_docs * case.n_trees * steps / (total_ms / 1e3),
+           "roofline": _roofline_hbm(case.n_docs, n_used, kern_ms, cfg)}
+    m.close()
+    return res
 
 
 def run_ours(args):
@@ -233,88 +309,121 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     import synth
     from paper_2205_07307_b200 import Model
+    from paper_2205_07307_b200.parallel import DocSharded, shard_bounds, tree_shard
 
-    tree_shard = args.shard == "trees"
-    case = _workload(args.config, 0 if tree_shard else rank)
-    if tree_shard:  # rank r holds trees [r*T/W, (r+1)*T/W) and scores every document
-        from paper_2205_07307_b200.parallel import tree_shard as _shard
-        fi, th, lv, _ = _shard(case.feature_index, case.thresholds, case.leaf_values, case.depth,
-                               ws, rank)
+    tree_mode = args.shard == "trees"
+    D = synth.CONFIGS[args.config]["n_docs"]
+    if tree_mode or ws == 1:
+        lo, hi = 0, D
+    else:
+        lo, hi = shard_bounds(D, ws, rank)
+    # rank 0 of a doc-sharded run also holds the whole batch for the bit-identity check
+    full_rows = ws == 1 or tree_mode or rank == 0
+    case = synth.make_case(args.config, rows=None if full_rows else (lo, hi))
+    if tree_mode:
+        fi, th, lv, _ = tree_shard(case.feature_index, case.thresholds, case.leaf_values, case.depth,
+                                   ws, rank)
         model = Model(fi, th, lv, case.depth, case.n_features, device=local)
     else:
         model = Model(case.feature_index, case.thresholds, case.leaf_values, case.depth,
                       case.n_features, device=local)
     info = model.info
-    x = torch.from_numpy(case.x).to(dev)
-    n = case.n_docs
+    off = 0 if full_rows else lo  # case.x holds rows [off, ...) of the batch
+    x_host = case.x[lo - off:hi - off]
+    x = torch.from_numpy(np.ascontiguousarray(x_host)).to(dev)
+    n = x.shape[0]
     out = torch.empty(n, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    ds = DocSharded(lambda t: model.score(t))
+    m_pad = DocSharded.padded_size(D, ws)
+    loc_pad = torch.zeros(m_pad, dtype=torch.float32, device=dev)
+    all_pad = torch.empty(m_pad * ws, dtype=torch.float32, device=dev)
 
     def step():
-        model.score(x, out=out, stream=stream)
-        if tree_shard and ws > 1:  # one NCCL all-reduce of the fp32 partial scores
-            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        if tree_mode:
+            model.score(x, out=out, stream=stream)
+            if ws > 1:  # one NCCL reduce (sum) of the fp32 partial scores to rank 0
+                dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
+        elif ws > 1:  # this rank's documents, then the NCCL all-gather of the scores
+            model.score(x, out=loc_pad[:n], stream=stream)
+            ds.gather_into(loc_pad, all_pad)
+        else:
+            model.score(x, out=out, stream=stream)
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        t0.record(stream)
-        for i in range(args.steps):
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
-        t1.record(stream)
-        torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    total_ms = t0.elapsed_time(t1)
-    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms, step_ms = _time_steps(step, args.steps, stream, ws, dev, clk)
 
-    # ---- two-stage path (binarize + apply), reported alongside ----
-    bins = torch.empty(model.bins_bytes(n), dtype=torch.uint8, device=dev)
-    for _ in range(max(1, args.warmup)):
-        model.binarize(x, out=bins, stream=stream)
-        model.apply(bins, n, out=out, stream=stream)
-    torch.cuda.synchronize()
-    k2 = max(1, min(args.steps, 200))
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    tb = ta = 0.0
-    for _ in range(k2):
-        ev[0].record(stream)
-        model.binarize(x, out=bins, stream=stream)
-        ev[1].record(stream)
-        model.apply(bins, n, out=out, stream=stream)
-        ev[2].record(stream)
+    # the fused kernel alone (one launch per step; the collective excluded) for the rooflines
+    kern_ms = step_ms
+    if ws > 1:
+        _, kern_ms = _time_steps(lambda: model.score(x, out=out, stream=stream),
+                                 max(3, min(args.steps, 50)), stream, 1, dev)
+
+    # ---- correctness of the sharded result (untimed) ----
+    check = None
+    if ws > 1:
         torch.cuda.synchronize()
-        tb += ev[0].elapsed_time(ev[1])
-        ta += ev[1].elapsed_time(ev[2])
-    tb /= k2
-    ta /= k2
+        if tree_mode:
+            step()
+            torch.cuda.synchronize()
+        if rank == 0:
+            if tree_mode:
+                full = Model(case.feature_index, case.thresholds, case.leaf_values, case.depth,
+                             case.n_features, device=local)
+                ref = full.score(x)
+                tol = 1e-5 * float(np.abs(case.leaf_values.astype(np.float64))
+                                   .reshape(case.n_trees, -1).max(1).sum())
+                err = float((out - ref).abs().max().item())
+                check = {"kind": "tree-shard sum vs one GPU", "max_abs_err": err, "tol": tol,
+                         "ok": err <= tol}
+                full.close()
+            else:
+                ref = model.score(torch.from_numpy(case.x).to(dev))
+                got = ds.unpad(all_pad, D)
+                same = bool(torch.equal(got.view(torch.int32), ref.view(torch.int32)))
+                check = {"kind": "doc-shard gather vs one GPU, whole batch", "bit_identical": same}
+
+    # ---- two-stage path (binarize + apply), one GPU, reported alongside ----
+    tb = ta = None
+    if ws == 1:
+        bins = torch.empty(model.bins_bytes(n), dtype=torch.uint8, device=dev)
+        for _ in range(max(1, args.warmup)):
+            model.binarize(x, out=bins, stream=stream)
+            model.apply(bins, n, out=out, stream=stream)
+        torch.cuda.synchronize()
+        k2 = max(1, min(args.steps, 20))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        tb = ta = 0.0
+        for _ in range(k2):
+            ev[0].record(stream)
+            model.binarize(x, out=bins, stream=stream)
+            ev[1].record(stream)
+            model.apply(bins, n, out=out, stream=stream)
+            ev[2].record(stream)
+            torch.cuda.synchronize()
+            tb += ev[0].elapsed_time(ev[1])
+            ta += ev[1].elapsed_time(ev[2])
+        tb /= k2
+        ta /= k2
+        del bins
 
     # ---- end to end through the public API from pinned host memory ----
-    xh = torch.from_numpy(case.x).pin_memory()
-    sh = torch.empty(n, dtype=torch.float32).pin_memory()
+    xh = torch.from_numpy(np.ascontiguousarray(x_host)).pin_memory()
+    if ws > 1 and not tree_mode:
+        sh = torch.empty(m_pad * ws, dtype=torch.float32).pin_memory()
+    else:
+        sh = torch.empty(n, dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        if tree_shard and ws > 1:  # H2D, shard scores, NCCL all-reduce, D2H
+        if ws > 1:  # H2D of this rank's inputs, score, collective, D2H of the result on rank 0
             x.copy_(xh, non_blocking=True)
             step()
-            sh.copy_(out, non_blocking=True)
+            if rank == 0:
+                sh.copy_(out if tree_mode else all_pad, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
-        else:
+        else:  # odf_score_host: chunked H2D / score / D2H over two streams
             model.score_host(xh, out=sh, chunk_docs=args.e2e_chunk)
 
     e2e_step()
@@ -329,43 +438,49 @@ def run_ours(args):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # bytes over all ranks: doc sharding copies each document once, tree sharding every
+    # document to every rank; the result read back is the [D] score vector on rank 0
+    h2d = int(D * x_host.shape[1] * 4) * (ws if tree_mode else 1)
+    d2h = int(D * 4)
 
-    line = None
     if rank == 0:
-        peak, peak_kind = _peaks()
-        docs_total = n * args.steps * (1 if tree_shard else ws)
+        docs_total = D * args.steps
         value = docs_total / (total_ms / 1000.0)
-        alg_bytes = n * (4 * info["n_used_features"] + 4)  # fused = 4*F_used + 4
-        achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
-        traffic, traffic_src = (args.traffic, "--traffic") if args.traffic else _traffic(args.config)
+        mhz = clk.summary().get("sm_mhz") or clk.max_mhz
         line = {
             "metric": METRIC, "value": value, "unit": "docs/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if tree_shard else "weak",
+            "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": synth.WORKLOAD_NAMES[args.config], "n_docs": n,
-                       "n_features": case.n_features, "n_trees": case.n_trees,
-                       "depth": case.depth, "used_features": info["n_used_features"],
-                       "path": "fused odf_score",
-                       "l2": "inputs larger than L2 (%.0f MB > 126 MB); no flush" % (case.x.nbytes / 1e6),
-                       "parallelism": (f"tree-shard x{ws} + NCCL all-reduce" if tree_shard
-                                       else f"doc-shard x{ws}")},
+            "config": _config(args.config, case, ws, args.shard, D),
+            "path": "fused odf_score (one launch per step)" +
+                    (" + NCCL reduce" if tree_mode and ws > 1 else
+                     " + NCCL all-gather" if ws > 1 else ""),
             "doc_trees_per_s": value * case.n_trees,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_kind": peak_kind, "kernel": "odf_main_kernel<FUSED,%d>" % case.depth,
-                         "kernel_ms": kern_ms, "alg_bytes_per_launch": alg_bytes},
-            "binding": _binding(args.config, kern_ms, info, clk),
-            "two_stage": {"binarize_ms": tb, "apply_ms": ta,
-                          "docs_per_s": n / ((tb + ta) / 1000.0)},
-            "e2e": {"value": n * k_e2e / e2e_s, "unit": "docs/s",
-                    "h2d_bytes_per_step": int(case.x.nbytes), "d2h_bytes_per_step": int(n * 4)},
+            "roofline": _roofline_hbm(n, info["n_used_features"], kern_ms, args.config),
+            "roofline_binding": _roofline_smem(args.config, kern_ms, info["num_sms"], mhz),
+            "e2e": {"value": D * k_e2e / e2e_s, "unit": "docs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": k_e2e,
+                    "path": "odf_score_host (pinned host memory, chunked H2D/score/D2H)"
+                            if ws == 1 else "H2D + odf_score + NCCL collective + D2H on rank 0"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "model": {k: info[k] for k in ("n_split_features", "n_columns", "trees_per_chunk",
-                                           "borders_in_smem", "stages_fused", "smem_fused",
-                                           "total_borders", "max_borders")},
+                                           "stages_fused", "smem_fused", "total_borders",
+                                           "max_borders")},
         }
+        if ws > 1:
+            line["per_rank_docs"] = n
+            line["check"] = check
+            line["fused_kernel_ms_rank0"] = kern_ms
+        if tb is not None:
+            line["two_stage"] = {"binarize_ms": tb, "apply_ms": ta,
+                                 "docs_per_s": n / ((tb + ta) / 1000.0)}
+        if ws == 1 and args.secondary != "none" and args.secondary != args.config:
+            del x
+            torch.cuda.empty_cache()
+            line["secondary"] = _secondary(args.secondary, max(3, min(args.steps * 10, 500)),
+                                           max(3, args.warmup), dev, stream)
         if not args.no_cpu_baseline and ws == 1:  # the oracle baseline: rank 0 at N=1 only
             line["cpu_baseline"] = cpu_baseline(case, target_s=args.ref_seconds)
         print(json.dumps(line), flush=True)
@@ -379,20 +494,22 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4"],
+                    help="default c3 (c4 with --shard trees)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shard", default="docs", choices=["docs", "trees"],
-                    help="multi-GPU: document sharding (weak scaling) or tree sharding + NCCL "
-                         "all-reduce of fp32 partials (strong scaling)")
-    ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--e2e-chunk", type=int, default=16384)
+                    help="multi-GPU: document sharding of one batch + all-gather, or tree "
+                         "sharding + NCCL reduce of fp32 partials (both strong scaling)")
+    ap.add_argument("--secondary", default="c2", help="second workload reported in the line, or none")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunk", type=int, default=65536)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "c4" if args.shard == "trees" else "c3"
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)

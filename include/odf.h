@@ -153,6 +153,9 @@ typedef struct {
     int32_t leaf_type;          /* ODF_LEAF_F32 / ODF_LEAF_U32 */
     int32_t bord_stride;        /* max bytes of one 32-factor sub-tile's border arrays */
     int32_t bins_elem_bytes;    /* 1: uint8 bins; 2: uint16 bins (a feature has > ODF_MAX_BORDERS) */
+    int32_t max_tile_docs;      /* 256 if 256-document tiles fit (odf_score_tiles), else 128 */
+    int32_t stages_fused_256;   /* ring stages of the fused kernel with 256-document tiles (0: none) */
+    int32_t smem_fused_256;     /* its dynamic shared memory per CTA, bytes (0: none) */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);
@@ -183,6 +186,24 @@ ODF_API odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t 
  * summation order); bins live only in shared memory, never in HBM.           */
 ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
                      float *d_scores, void *stream);
+
+/* Documents per tile (a performance choice, not a numerical one).  odf_score and
+ * odf_apply pick it themselves; these variants take tile_docs = 0 (the same
+ * automatic choice), 128 or 256.  A 256-document tile is two 128-document halves
+ * that share every tree chunk staged in shared memory, which halves the forest's
+ * L2 -> shared-memory traffic per document (what binds deep forests, BASELINE
+ * config c4); it needs two code blocks in shared memory, so it exists only for
+ * fp32-leaf models without > 254-border factors whose codes fit
+ * (odf_model_info.max_tile_docs).  The automatic choice takes it for depth >= 7
+ * and at least 2 x num_sms tiles of 256 documents (odf_score: only when its ring
+ * still has >= 3 slots, stages_fused_256).  Scores are bit-identical for
+ * every tile width (the summation order of DESIGN.md does not depend on it).
+ * Errors: as odf_score / odf_apply; ODF_E_INVALID_ARG for another tile_docs;
+ * ODF_E_UNSUPPORTED if 256 is requested and max_tile_docs is 128.            */
+ODF_API odf_status odf_score_tiles(const odf_model *m, const float *d_factors, int64_t n_docs,
+                                   int64_t ld, float *d_scores, int32_t tile_docs, void *stream);
+ODF_API odf_status odf_apply_tiles(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,
+                                   float *d_scores, int32_t tile_docs, void *stream);
 
 /* Feature-major input (NEXT-4; the paper's pre-transposed variant, §5.5):
  * d_factors_fm [n_features x ld_fm] fp32 row-major, i.e. factor f of document i at

@@ -14,7 +14,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libodf.so")
-SOURCES = ["odf_capi.cu", "odf_kernels.cu"]
+# one kernel family per translation unit (odf_kernels.cuh holds the templates), so
+# the objects compile in parallel
+SOURCES = ["odf_capi.cu", "odf_k_fused_nf.cu", "odf_k_fused_nu.cu", "odf_k_fused_wf.cu",
+           "odf_k_fused_wu.cu", "odf_k_apply.cu", "odf_k_halves.cu", "odf_k_aux.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -29,7 +32,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "odf.h")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "odf.h"),
+                                                                 os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -39,12 +43,13 @@ def _compile_link(out: str, defines=(), verbose: bool = False) -> None:
     source and headers."""
     import hashlib
     from concurrent.futures import ThreadPoolExecutor
-    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xfatbin", "-compress-all",
+              "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
               *[f"-D{d}" for d in defines]]
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
-    headers = sorted([os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")] +
+    headers = sorted([os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] +
                      [os.path.join(ROOT, "include", "odf.h")])
 
     def key(src):  # flags + the bytes of the source and every header it may include

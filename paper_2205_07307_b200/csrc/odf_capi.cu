@@ -13,7 +13,9 @@
 //    "code >= K" on column A with K = k+1 when k+1 <= 127, else on column B
 //    with K = k-126;  level descriptor = (col << 19) | (128-K)  (odf_internal.h);
 //  * leaf tables reversed (table[F] = leaf[2^d-1-F]) because the kernels
-//    assemble the complemented index F (flags are "condition false");
+//    assemble the complemented index F (flags are "condition false"), and
+//    bank-swizzled (leaf_pos: words sharing a shared-memory bank are far apart
+//    in Hamming distance, so a warp's gathers conflict less);
 //  * trees grouped in chunks of tc (multiple of 16) = [descriptors | tables].
 #include <algorithm>
 #include <cmath>
@@ -59,16 +61,21 @@ odf_status cuda_fail(cudaError_t e, const char *what)
 }
 
 uint32_t skew_h(uint32_t p) { return p + (p >> 5); }  // as skew() in odf_kernels.cu
+
+// Bank-swizzled table position of the complemented leaf index F (as leaf_addrs /
+// swz_bank_hi in odf_kernels.cu): row F >> 5 keeps its 32 words, the bank of
+// word F is L ^ (H ? 31 : 0) at depth 6 and L ^ H ^ (parity(H) ? 31 : 0) at
+// depth 7..10 (F = 32 H + L); tables of <= 32 words are conflict-free as they are.
+uint32_t leaf_pos(int depth, uint32_t F)
+{
+    const uint32_t H = F >> 5, L = F & 31u;
+    if (depth <= 5) return F;
+    if (depth == 6) return (H << 5) | (L ^ (H ? 31u : 0u));
+    const uint32_t par = static_cast<uint32_t>(__builtin_popcount(H) & 1);
+    return (H << 5) | ((L ^ H ^ (par ? 31u : 0u)) & 31u);
+}
 constexpr uint32_t kExtraShiftH = 4;  // fmeta.y bits 4-7 = code columns - 1 (as kExtraShift)
 uint32_t align_up(uint64_t v, uint64_t a) { return static_cast<uint32_t>((v + a - 1) / a * a); }
-// Ring-geometry tuning knobs (diagnostics sweeps; unset = the built-in policy):
-// ODF_RING_SUBS = factor sub-tiles per fused ring slot (1 or 2), ODF_RING_STAGES_MAX.
-int env_int(const char *name, int dflt)
-{
-    const char *v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
-}
-
 struct Plan {
     uint32_t off_bins = 0, off_ring = 0, off_red = 0, off_bars = 0;
     uint32_t slot_bytes = 0, off_meta = 0, off_bord = 0;
@@ -76,6 +83,10 @@ struct Plan {
     uint32_t off_stage = 0;  // wide models, apply: u16 bins staging
     size_t smem = 0;
     int grid_per_sm = 1;
+    int halves = 1;              // tile = halves x 128 documents
+    uint32_t half_stride = 0;    // bytes between the halves' code blocks
+    uint32_t hdesc_bytes = 0;    // halves == 2: tables' offset in a half-chunk ring slot
+    bool valid = false;
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -108,6 +119,7 @@ struct odf_model {
     bool leaf_u32 = false;
     double scale = 1.0, bias = 0.0;
     Plan fused, binz, apply;
+    Plan fused2, apply2;  // 256-document tiles (two halves), when they fit
     // odf_score_host staging
     std::mutex host_mu;
     float *d_stage[2] = {nullptr, nullptr};
@@ -122,49 +134,59 @@ namespace {
 // ----------------------------------------------------------------------------
 // shared-memory plans
 // ----------------------------------------------------------------------------
-bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
+bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int halves = 1)
 {
-    // code columns + the trash column (stores of unused pair slots); the binarize
-    // kernel of a wide model stores u16 bins; the apply kernel of a wide model
-    // stages the u16 bins tile next to the code columns it expands them into
+    // code columns + the trash column (stores of unused pair slots), one block per
+    // tile half; the binarize kernel of a wide model stores u16 bins; the apply kernel
+    // of a wide model stages the u16 bins tile next to the code columns it expands
+    // them into
     const uint32_t elem = (mode == MODE_BINARIZE && m.wide) ? 2u : 1u;
-    const uint32_t bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile * elem, 1024);
+    const uint32_t half_bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile * elem, 1024);
+    const uint32_t bins = half_bins * static_cast<uint32_t>(halves);
     const uint32_t stage = (mode == MODE_APPLY && m.wide)
                                ? align_up(static_cast<uint64_t>(m.n_used) * kTile * 2, 1024) : 0u;
-    const uint32_t red_bytes = m.leaf_u32 ? 2 * kRedBytes : kRedBytes;
+    const uint32_t red_bytes = (m.leaf_u32 ? 2 * kRedBytes : kRedBytes) * static_cast<uint32_t>(halves);
     const uint32_t bins_region = ((mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes)) + stage;
     const uint32_t bars = align_up(160 + 8u * m.n_fchunks, 128);  // barriers, scratch, bchunk copy
-    // a factor sub-tile travels as [16 KB box][512 B fmeta][its border arrays]
-    const uint32_t unit = kFSubBytes + kMetaBytes + m.bord_stride;
+    // a factor sub-tile travels as [halves x 16 KB boxes][512 B fmeta][its border arrays]
+    const uint32_t unit = kFSubBytes * halves + kMetaBytes + m.bord_stride;
+    // tree jobs: whole chunks, or (halves == 2) half-chunks of tc / 2 trees
+    uint32_t hdesc = 0, tree_slot;
+    if (halves == 1) {
+        tree_slot = align_up(m.chunk_bytes, 1024);
+    } else {
+        hdesc = align_up(static_cast<uint64_t>(m.tc / 2) * desc_stride(m.depth), 256);
+        tree_slot = align_up(hdesc + static_cast<uint64_t>(m.tc / 2) * m.table_stride, 1024);
+    }
     uint32_t slot;
     int smax;
     if (mode == MODE_BINARIZE) {
         slot = align_up(unit, 1024);
         smax = 6;
     } else if (mode == MODE_APPLY) {
-        slot = align_up(m.chunk_bytes, 1024);
+        slot = tree_slot;
         smax = 4;
     } else {
-        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024),
-                                  align_up((env_int("ODF_RING_SUBS", 1) == 1 ? 1u : 2u) * unit, 1024));
-        smax = env_int("ODF_RING_STAGES_MAX", 8);
+        slot = std::max<uint32_t>(tree_slot, align_up(unit, 1024));
+        smax = 8;
     }
     const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024;
     const int64_t fixed = static_cast<int64_t>(bins_region) + bars;
-    if (mode == MODE_FUSED && (avail - fixed) / slot < 2)  // fall back to one sub-tile per slot
-        slot = std::max<uint32_t>(align_up(m.chunk_bytes, 1024), align_up(unit, 1024));
-    pl.stages = std::min<int64_t>(smax, (avail - fixed) / slot);
+    pl.stages = static_cast<int>(std::min<int64_t>(smax, (avail - fixed) / slot));
     if (pl.stages < 2) {
         char b[256];
         snprintf(b, sizeof b,
-                 "shared memory: %d code columns x 128 B + 2 x %u B slots do not fit %d B", m.n_cols,
-                 slot, m.max_smem);
+                 "shared memory: %d x %d code columns x 128 B + 2 x %u B slots do not fit %d B", halves,
+                 m.n_cols, slot, m.max_smem);
         why = b;
         return false;
     }
+    pl.halves = halves;
+    pl.half_stride = half_bins;
+    pl.hdesc_bytes = hdesc;
     pl.slot_bytes = slot;
     pl.fsub = std::max<int>(1, static_cast<int>(slot / unit));
-    pl.off_meta = pl.fsub * kFSubBytes;
+    pl.off_meta = pl.fsub * halves * kFSubBytes;
     pl.off_bord = pl.off_meta + pl.fsub * kMetaBytes;
     uint32_t off = 0;
     pl.off_ring = off;                    // ring first: TMA swizzle needs 1024 B alignment
@@ -176,6 +198,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why)
     pl.off_bars = off;
     off += bars;
     pl.smem = off;
+    pl.valid = true;
     return true;
 }
 
@@ -243,6 +266,8 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.off_meta = pl.off_meta;
     p.off_bord = pl.off_bord;
     p.bord_stride = m->bord_stride;
+    p.half_stride = pl.half_stride;
+    p.hdesc_bytes = pl.hdesc_bytes;
     return p;
 }
 
@@ -274,6 +299,32 @@ int grid_for(const odf_model *m, const Plan &pl, int64_t n_tiles)
 {
     const int64_t g = static_cast<int64_t>(m->num_sms) * pl.grid_per_sm;
     return static_cast<int>(std::min<int64_t>(n_tiles, g));
+}
+
+// Tile width of a fused / apply launch (odf.h "Documents per tile"): 0 = automatic.
+// Returns the halves (1 or 2) or 0 after setting the error.
+int choose_halves(const odf_model *m, int mode, int64_t n_docs, int32_t tile_docs, odf_status *st)
+{
+    const Plan &p2 = mode == MODE_FUSED ? m->fused2 : m->apply2;
+    *st = ODF_OK;
+    if (tile_docs == 0) {
+        // 256-document tiles halve the forest's L2 -> shared-memory bytes per document
+        // but, next to two code blocks, leave fewer ring slots: the tree stream is then
+        // bound by the bytes it has in flight.  Measured on c4 (depth 10, 2 slots):
+        // apply 25.9 -> 22.7 ms, fused (its slots also carry 2-box factor jobs)
+        // 28.4 -> 32.4 ms; so fused takes them only with >= 3 slots.
+        const int64_t tiles256 = (n_docs + 2 * kTile - 1) / (2 * kTile);
+        const bool deep = m->depth >= 7 && tiles256 >= 2 * static_cast<int64_t>(m->num_sms);
+        return (p2.valid && deep && (mode == MODE_APPLY || p2.stages >= 3)) ? 2 : 1;
+    }
+    if (tile_docs == kTile) return 1;
+    if (tile_docs == 2 * kTile) {
+        if (p2.valid) return 2;
+        *st = fail(ODF_E_UNSUPPORTED, "256-document tiles do not fit this model (max_tile_docs = 128)");
+        return 0;
+    }
+    *st = fail(ODF_E_INVALID_ARG, "tile_docs = %d not in {0, 128, 256}", tile_docs);
+    return 0;
 }
 
 }  // namespace
@@ -586,20 +637,11 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     // chunk size: about one factor sub-tile (16.5 KB + its borders), so one ring slot
     // carries a sub-tile in phase A or a chunk of similar bytes in phase B and the
     // ring is as deep as shared memory allows (up to 8 stages: more factor data in
-    // flight while phase A runs); ODF_RING_SUBS=2 selects two-sub-tile slots
+    // flight while phase A runs); at least 16 trees (one per consumer warp)
     {
-        int max_smem = 0;
-        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
-        const int64_t bins = std::max<int64_t>(align_up(static_cast<uint64_t>(m->n_cols + 1) * kTile, 1024),
-                                               2 * kRedBytes);
-        const int64_t room = static_cast<int64_t>(max_smem) - 1024 - 1024 - bins;  // for >= 2 slots
-        uint32_t target = 20480u;
-        const int subs = env_int("ODF_RING_SUBS", 1);
-        if (subs == 1) target = unit;
-        else if (room / 2 >= static_cast<int64_t>(align_up(2u * unit, 1024))) target = 2u * unit;
         const uint32_t per = static_cast<uint32_t>(dstride) + m->table_stride;
-        m->tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, target / (16u * per)));
+        m->tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, unit / (16u * per)));
     }
     m->desc_bytes = align_up(static_cast<uint64_t>(m->tc) * dstride, 256);
     m->chunk_bytes = m->desc_bytes + static_cast<uint32_t>(m->tc) * m->table_stride;
@@ -629,14 +671,21 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
             const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
                                         : static_cast<uint32_t>(colB_of[f]) + c - 1u;
             const uint32_t K = k - 127u * c + 1u;
-            desc[l] = (col << 19) | (128u - K);
+            if (ODF_DESC8) {
+                desc[2 * l] = col * kTile;
+                desc[2 * l + 1] = (128u - K) * 0x01010101u;
+            } else {
+                desc[l] = (col << 19) | (128u - K);
+            }
         }
         float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
         if (u32) {
             uint32_t *tab_u = reinterpret_cast<uint32_t *>(tab);
-            for (uint32_t F = 0; F < nleaf; ++F) tab_u[F] = leaf_u[t * nleaf + (nleaf - 1 - F)];
+            for (uint32_t F = 0; F < nleaf; ++F)
+                tab_u[leaf_pos(depth, F)] = leaf_u[t * nleaf + (nleaf - 1 - F)];
         } else {
-            for (uint32_t F = 0; F < nleaf; ++F) tab[F] = leaf_f[t * nleaf + (nleaf - 1 - F)];
+            for (uint32_t F = 0; F < nleaf; ++F)
+                tab[leaf_pos(depth, F)] = leaf_f[t * nleaf + (nleaf - 1 - F)];
         }
     }
 
@@ -700,6 +749,13 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         return fail(ODF_E_UNSUPPORTED, "%s", why.c_str());
     }
     m->binz.grid_per_sm = occupancy_main(MODE_BINARIZE, 0, m->binz.smem);
+    // 256-document tiles (two halves), fp32 narrow models, when two code blocks fit
+    if (!m->leaf_u32 && !m->wide) {
+        std::string why2;
+        if (!make_plan(*m, MODE_FUSED, m->fused2, why2, 2)) m->fused2 = Plan();
+        if (!make_plan(*m, MODE_APPLY, m->apply2, why2, 2)) m->apply2 = Plan();
+        if (!m->fused2.valid || !m->apply2.valid) m->fused2 = m->apply2 = Plan();  // both or neither
+    }
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         odf_free_model(m.release());
@@ -731,6 +787,9 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->leaf_type = m->leaf_u32 ? ODF_LEAF_U32 : ODF_LEAF_F32;
     info->bord_stride = static_cast<int32_t>(m->bord_stride);
     info->bins_elem_bytes = m->wide ? 2 : 1;
+    info->max_tile_docs = m->fused2.valid ? 2 * kTile : kTile;
+    info->stages_fused_256 = m->fused2.valid ? m->fused2.stages : 0;
+    info->smem_fused_256 = m->fused2.valid ? static_cast<int32_t>(m->fused2.smem) : 0;
     return ok();
 }
 
@@ -748,12 +807,14 @@ odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
 
 static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64_t n_docs, int64_t ld,
                            const uint8_t *bins_in, uint8_t *bins_out, float *scores, cudaStream_t s,
-                           uint64_t *sums = nullptr, double *dscores = nullptr, bool fm = false)
+                           uint64_t *sums = nullptr, double *dscores = nullptr, bool fm = false,
+                           int halves = 1)
 {
-    const Plan &pl = mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
+    const Plan &pl = halves == 2 ? (mode == MODE_FUSED ? m->fused2 : m->apply2)
+                                 : mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
     KParams p = base_params(m, pl);
     p.n_docs = n_docs;
-    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.n_tiles = (n_docs + kTile * halves - 1) / (kTile * halves);
     p.bins_in = bins_in;
     p.bins_out = bins_out;
     p.scores = scores;
@@ -770,7 +831,7 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != m->device) cudaSetDevice(m->device);
-    cudaError_t e = launch_main(mode, m->depth, p, tmp, grid_for(m, pl, p.n_tiles), pl.smem, s);
+    cudaError_t e = launch_main(mode, m->depth, p, tmp, grid_for(m, pl, p.n_tiles), pl.smem, s, halves);
     if (prev != m->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     return ok();
@@ -791,29 +852,46 @@ odf_status odf_binarize(const odf_model *m, const float *d_factors, int64_t n_do
 odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, float *d_scores,
                      void *stream)
 {
+    return odf_apply_tiles(m, d_bins, n_docs, d_scores, 0, stream);
+}
+
+odf_status odf_apply_tiles(const odf_model *m, const uint8_t *d_bins, int64_t n_docs, float *d_scores,
+                           int32_t tile_docs, void *stream)
+{
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
     if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "integer-leaf model: use odf_apply_u64");
     if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
+    odf_status st;
+    const int halves = choose_halves(m, MODE_APPLY, n_docs, tile_docs, &st);
+    if (!halves) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
     if (m->n_used > 0 && !d_bins) return fail(ODF_E_INVALID_ARG, "d_bins is NULL");
     if (reinterpret_cast<uintptr_t>(d_bins) % 16 != 0)
         return fail(ODF_E_INVALID_ARG, "d_bins not 16-byte aligned");
     return run_main(m, MODE_APPLY, nullptr, n_docs, 0, d_bins, nullptr, d_scores,
-                    static_cast<cudaStream_t>(stream));
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr, false, halves);
 }
 
 odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
                      float *d_scores, void *stream)
 {
+    return odf_score_tiles(m, d_factors, n_docs, ld, d_scores, 0, stream);
+}
+
+odf_status odf_score_tiles(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                           float *d_scores, int32_t tile_docs, void *stream)
+{
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
     if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "integer-leaf model: use odf_score_u64");
     odf_status st = check_factors(m, d_factors, n_docs, ld);
     if (st != ODF_OK) return st;
+    const int halves = choose_halves(m, MODE_FUSED, n_docs, tile_docs, &st);
+    if (!halves) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
     return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, d_scores,
-                    static_cast<cudaStream_t>(stream));
+                    static_cast<cudaStream_t>(stream), nullptr, nullptr, false, halves);
 }
 
 odf_status odf_binarize_fm(const odf_model *m, const float *d_factors_fm, int64_t n_docs,

@@ -25,8 +25,14 @@ constexpr uint32_t kNoCol = 0xFFFFFFFFu;
 // so the apply loop has a fixed trip count.
 // Level descriptor (u32): bits 19-31 = code column (col * 128 = desc >> 12), bits 0-7 =
 // 128 - K; a tree's descriptors are padded to a multiple of 4 levels (LDS.128 groups).
+#ifndef ODF_DESC8
+#define ODF_DESC8 0  // 1: 8-byte level descriptors {col * 128, (128 - K) * 0x01010101} (A/B builds)
+#endif
 constexpr int kMaxDescCol = 8191;
-__host__ __device__ constexpr int desc_stride(int depth) { return ((depth + 3) & ~3) * 4; }
+__host__ __device__ constexpr int desc_stride(int depth)
+{
+    return ODF_DESC8 ? ((depth + 1) & ~1) * 8 : ((depth + 3) & ~3) * 4;
+}
 __host__ __device__ constexpr int table_stride(int depth) { return depth <= 6 ? 256 : (4 << depth); }
 __host__ __device__ constexpr int trees_per_chunk(int depth)
 {
@@ -77,6 +83,8 @@ struct KParams {
     uint32_t off_bins, off_ring, off_red, off_bars;
     uint32_t slot_bytes;
     uint32_t off_meta, off_bord, bord_stride;  // within a factor job's slot
+    uint32_t half_stride;    // tile halves (H = 2): bytes between the halves' code blocks
+    uint32_t hdesc_bytes;    // H = 2: offset of the tables in a half-chunk ring slot
     int32_t stages;
     int32_t fsub_per_job;    // factor sub-tiles per job (tiles, then metas, then borders)
     // ---- latency path (K4) workspace ----
@@ -96,8 +104,18 @@ struct KParams {
     uint64_t *fp_out;
 };
 
+// Kernel pointers, one kernel family per translation unit (odf_k_*.cu).
+const void *kptr_fused_nf(int depth);  // fused, fp32 leaves
+const void *kptr_fused_nu(int depth);  // fused, u32 leaves (NEXT-1)
+const void *kptr_fused_wf(int depth);  // fused, wide models (NEXT-4), fp32 leaves
+const void *kptr_fused_wu(int depth);  // fused, wide models, u32 leaves
+const void *kptr_apply(int depth, bool u32);
+const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
+const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
+const void *kptr_binarize(bool wide);
+
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
-                        size_t smem, cudaStream_t s);
+                        size_t smem, cudaStream_t s, int halves = 1);
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
                          cudaStream_t s);
 cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,

@@ -1,4 +1,5 @@
-// odf_kernels.cu -- sm_100a kernels of the oblivious-forest hot path.
+// odf_kernels.cuh -- sm_100a kernels of the oblivious-forest hot path (templates;
+// instantiated by odf_k_*.cu, one kernel family per translation unit so they build in parallel).
 //
 //   K1 binarize   fp32 factors (TMA-staged, 128B-swizzled tiles) -> uint8 bins
 //   K2 apply      bins -> per-document fp32 scores
@@ -25,6 +26,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#pragma once
 #include "odf_internal.h"
 
 #ifndef ODF_DIAG
@@ -35,7 +37,7 @@ namespace odf {
 
 #if ODF_DIAG & 8  // diagnostics build only: per-warp phase timeline (tools/timeline.py)
 constexpr int kDiagIt = 64;  // tile iterations recorded per CTA
-__device__ unsigned long long g_diag[148 * kDiagIt * 16 * 8];
+static __device__ unsigned long long g_diag[148 * kDiagIt * 16 * 8];
 __device__ __forceinline__ unsigned long long gtime()
 {
     unsigned long long t;
@@ -248,6 +250,7 @@ __device__ __forceinline__ uint32_t neg_npad(const uint4 &m)
 struct SmemSink {
     uint32_t base;
     __device__ __forceinline__ void st(uint32_t off, uint32_t v) const { sts_u8(base + off, v); }
+    __device__ __forceinline__ SmemSink at(uint32_t off) const { return SmemSink{base + off}; }
 };
 struct GmemSink {
     uint8_t *base;
@@ -263,6 +266,7 @@ struct SmemSink16 {
     {
         sst<uint16_t>(base + 2u * off, static_cast<uint16_t>(v));
     }
+    __device__ __forceinline__ SmemSink16 at(uint32_t off) const { return SmemSink16{base + off}; }
 };
 
 // Both factors of a pair: one warp-uniform test for code-column splits per pair.
@@ -514,12 +518,33 @@ __device__ __forceinline__ void tree_level(uint32_t dsc, uint32_t lane_bins, int
         hi = (l == 8) ? s : ((hi >> 1) | s);
 }
 
+// 8-byte descriptors (ODF_DESC8): {col * 128, (128 - K) replicated in every byte}
+template <int DEPTH>
+__device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, uint32_t lane_bins, int l,
+                                            uint32_t &lo, uint32_t &hi)
+{
+    const uint32_t w = ldsa_u32(lane_bins + col128);
+    const uint32_t s = (w + krep) & 0x80808080u;
+    if (l < 8)
+        lo = (l == 0) ? s : ((lo >> 1) | s);
+    else
+        hi = (l == 8) ? s : ((hi >> 1) | s);
+}
+
 template <int DEPTH>
 __device__ __forceinline__ void tree_flags(uint32_t d, uint32_t lane_bins, uint32_t &lo,
                                            uint32_t &hi)
 {
     lo = 0;
     hi = 0;
+#if ODF_DESC8
+#pragma unroll
+    for (int l = 0; l < DEPTH; l += 2) {  // one LDS.128 per two levels
+        const uint4 q = lds_v4u(d + l * 8);
+        tree_level8<DEPTH>(q.x, q.y, lane_bins, l, lo, hi);
+        if (l + 1 < DEPTH) tree_level8<DEPTH>(q.z, q.w, lane_bins, l + 1, lo, hi);
+    }
+#else
 #pragma unroll
     for (int l = 0; l < DEPTH; l += 4) {
         if (l + 2 < DEPTH) {  // 3 or 4 levels left: one LDS.128 (padding levels unused)
@@ -536,6 +561,7 @@ __device__ __forceinline__ void tree_flags(uint32_t d, uint32_t lane_bins, uint3
             tree_level<DEPTH>(lds_u32(d + l * 4), lane_bins, l, lo, hi);
         }
     }
+#endif
 }
 
 // Complemented leaf index F of the lane's 4 documents.
@@ -557,8 +583,28 @@ __device__ __forceinline__ void tree_findex(uint32_t d, uint32_t lane_bins, uint
     }
 }
 
-// Absolute shared-window addresses of the 4 leaves (tables reversed; tb = the
-// table base, absolute and 256-aligned).
+// Bank-swizzled leaf tables (model compiler: leaf_pos in odf_capi.cu).  A warp's
+// 32 gathers from one table conflict when two lanes want different words of one
+// bank; with 2^d > 32 words a bank holds several.  Leaf indices are skewed (a
+// level's condition is mostly true or mostly false), so popular indices differ in
+// few bits: the words sharing a bank are chosen FAR apart in Hamming distance.
+// With F = H * 32 + L (L = the 5 low bits), word F is stored at bank
+//   depth 6:      L ^ (H ? 31 : 0)          (F shares its bank only with F ^ 63)
+//   depth 7..10:  L ^ H ^ (parity(H) ? 31 : 0)  (a [d, 5] code of distance 4: two
+//                 indices in one bank differ in >= 4 bits)
+// and row H.  Simulated on the c3/c4 models: 1.90 -> 1.21 (depth 6) and 5.5 ->
+// 2.3 (depth 10) wavefronts per warp gather.  Here: 4 documents per lane, lo =
+// F's low 8 bits per byte, h = F's bits 8.. per byte; rewrites lo's 5 low bits.
+__device__ __forceinline__ uint32_t swz_bank_hi(uint32_t lo, uint32_t h)
+{
+    const uint32_t g = ((lo >> 5) & 0x07070707u) | (h << 3);  // H per byte (<= 5 bits)
+    const uint32_t x = g ^ (g >> 1) ^ (g >> 2);                // bit 0: g0^g1^g2
+    const uint32_t par = (x ^ (x >> 3)) & 0x01010101u;         // bit 0: parity(H)
+    return lo ^ g ^ (par * 31u);
+}
+
+// Absolute shared-window addresses of the 4 leaves (tables reversed and
+// bank-swizzled; tb = the table base, absolute and 256-aligned).
 template <int DEPTH>
 __device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint32_t tb,
                                            uint32_t a[4])
@@ -568,13 +614,18 @@ __device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint3
     if constexpr (DEPTH <= 6) {
         // byte = F << (8-DEPTH); want 4F in the low byte of a 256-aligned base
         if constexpr (DEPTH < 6 && DEPTH > 0) lo >>= (6 - DEPTH);
+        // depth 6: byte bit 7 = F bit 5 -> complement F's 5 low bits (byte bits 2..6)
+        if constexpr (DEPTH == 6) lo ^= prmt(lo, 0u, 0xBA98u) & 0x7C7C7C7Cu;
 #pragma unroll
         for (int n = 0; n < 4; ++n) a[n] = prmt(lo, tb, 0x7650u | n);
     } else if constexpr (DEPTH <= 8) {
+        if constexpr (DEPTH == 7) lo = (lo >> 1) & 0x7F7F7F7Fu;  // byte = F
+        lo = swz_bank_hi(lo, 0u);
 #pragma unroll
-        for (int n = 0; n < 4; ++n) a[n] = tb + (prmt(lo, 0u, 0x4440u | n) << (DEPTH - 6));
+        for (int n = 0; n < 4; ++n) a[n] = tb + (prmt(lo, 0u, 0x4440u | n) << 2);
     } else {
         const uint32_t h = hi >> (16 - DEPTH);
+        lo = swz_bank_hi(lo, h);
 #pragma unroll
         for (int n = 0; n < 4; ++n)
             a[n] = tb + (prmt(lo, h, 0xCC00u | ((4u + n) << 4) | n) << 2);
@@ -620,9 +671,11 @@ struct Acc<false> {
                      ::"r"(x), "r"(sabs(scratch)) : "memory");
     }
     static constexpr uint32_t kRed = kRedBytes;
-    __device__ __forceinline__ void to_red(uint32_t red, int warp, int lane) const
+    // reduction buffer [16 groups][tile_docs]: group g's partials of the lane's 4
+    // documents (doc0 = the first document's position in the tile)
+    __device__ __forceinline__ void to_red(uint32_t red, int g, int doc0, int tile_docs) const
     {
-        sts_v4f(red + warp * (kTile * 4) + lane * 16, v[0], v[1], v[2], v[3]);
+        sts_v4f(red + (g * tile_docs + doc0) * 4, v[0], v[1], v[2], v[3]);
     }
 };
 template <>
@@ -640,9 +693,9 @@ struct Acc<true> {
                      ::"r"(x), "r"(sabs(scratch)) : "memory");
     }
     static constexpr uint32_t kRed = 2 * kRedBytes;
-    __device__ __forceinline__ void to_red(uint32_t red, int warp, int lane) const
+    __device__ __forceinline__ void to_red(uint32_t red, int g, int doc0, int tile_docs) const
     {
-        const uint32_t a = red + warp * (kTile * 8) + lane * 32;
+        const uint32_t a = red + (g * tile_docs + doc0) * 8;
         sst<ulonglong2>(a, make_ulonglong2(v[0], v[1]));
         sst<ulonglong2>(a + 16, make_ulonglong2(v[2], v[3]));
     }
@@ -681,21 +734,22 @@ __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes,
     }
 }
 
-// Fixed-order combine of the 16 warp partials of document tid (< 128) and store.
+// Fixed-order combine of the 16 group partials of document tid (< tile_docs) and store:
+// score = (((P_0 + P_1) + P_2) + ... + P_15).
 __device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int tid, int64_t doc,
-                                           Acc<false> *)
+                                           int tile_docs, Acc<false> *)
 {
     float s = lds_f32(red + tid * 4);
 #pragma unroll
-    for (int w = 1; w < kConsumerWarps; ++w) s += lds_f32(red + w * (kTile * 4) + tid * 4);
+    for (int g = 1; g < kConsumerWarps; ++g) s += lds_f32(red + (g * tile_docs + tid) * 4);
     if (doc < p.n_docs) p.scores[doc] = s;
 }
 __device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int tid, int64_t doc,
-                                           Acc<true> *)
+                                           int tile_docs, Acc<true> *)
 {
     unsigned long long r = 0;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) r += sld<unsigned long long>(red + w * (kTile * 8) + tid * 8);
+    for (int g = 0; g < kConsumerWarps; ++g) r += sld<unsigned long long>(red + (g * tile_docs + tid) * 8);
     if (doc < p.n_docs) {
         if (p.sums) p.sums[doc] = r;
         // (R - 2^31) * S + B, rounded op by op (no FMA contraction)
@@ -741,12 +795,15 @@ __device__ __forceinline__ void expand_wide(const KParams &p, uint32_t stage, ui
 }
 
 // Phase A of one tile: the tile's factor jobs from the ring (slot / phase carried
-// across phases and tiles).  Warp w binarizes quad w >> 1 of every sub-tile for
-// documents 64 * (w & 1) + lane (+ 32).  Parameters are read once into registers.
-template <bool CODES, bool WIDE, bool FM, class Sink>
+// across phases and tiles).  A job's slot holds, per 32-factor sub-tile, H boxes of
+// 128 documents (one per tile half), then the sub-tiles' fmeta, then their border
+// arrays.  Warp w binarizes quad w >> 1 of every box for documents 64 * (w & 1) +
+// lane (+ 32); the codes of half h go to the code block at h * half_stride.  Only
+// the tile's hv halves that hold documents are loaded and binarized.
+template <bool CODES, bool WIDE, bool FM, int H, class Sink>
 __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint32_t ring, uint32_t bars,
                                         int n_fjobs, int S, int warp, int lane, uint32_t &slot,
-                                        uint32_t &ph, unsigned long long &wait_ns)
+                                        uint32_t &ph, unsigned long long &wait_ns, int hv)
 {
     const int fsub = p.fsub_per_job, n_fchunks = p.n_fchunks;
     const uint32_t slot_bytes = p.slot_bytes, off_meta = p.off_meta, off_bord = p.off_bord,
@@ -766,9 +823,17 @@ __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint3
 #if ODF_DIAG & 1  // diagnostics build only: phase A does no work (TMA streaming rate)
         if (nsub < 0)
 #endif
-        for (int s = 0; s < nsub; ++s)
-            binarize_sub<2, CODES, WIDE, FM>(sb + s * kFSubBytes, sb + off_meta + s * kMetaBytes,
-                                             sb + off_bord + s * bord_stride, sink, q, dbase, lane);
+        for (int s = 0; s < nsub; ++s) {
+            if constexpr (H == 1) {
+                binarize_sub<2, CODES, WIDE, FM>(sb + s * kFSubBytes, sb + off_meta + s * kMetaBytes,
+                                                 sb + off_bord + s * bord_stride, sink, q, dbase, lane);
+            } else {
+                for (int h = 0; h < hv; ++h)
+                    binarize_sub<2, CODES, WIDE, FM>(sb + (s * H + h) * kFSubBytes, sb + off_meta + s * kMetaBytes,
+                                                     sb + off_bord + s * bord_stride, sink.at(h * p.half_stride),
+                                                     q, dbase, lane);
+            }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty);
         if (++slot == static_cast<uint32_t>(S)) {
@@ -782,13 +847,35 @@ __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint3
 // Main persistent kernel: MODE_FUSED (K3), MODE_BINARIZE (K1), MODE_APPLY (K2)
 // WIDE: model with > 254 borders on some factor (NEXT-4): the wide search path in
 // phase A, and u16 true bins from MODE_BINARIZE.
+// H: tile halves.  A tile is H x 128 documents; each half has its own code block
+// [n_cols + 1][128] (half_stride bytes apart), built from its own TMA box per
+// factor sub-tile.  H = 2 (fused / apply, fp32 narrow models) lets one staged tree
+// chunk serve 256 documents: half the L2 -> shared-memory forest traffic per
+// document, which binds deep forests (c4: 16.6 MB of depth-10 tables per tile).
+// Phase B with H = 2: warp w applies tree slot j = w & 7 of every half-chunk
+// (tc / 2 trees, one ring slot) to half w >> 3.  A warp's trees are then t = j, j+8,
+// j+16, ... of the forest, whose summation groups t mod 16 alternate j, j+8, j, ...,
+// so two accumulators (swapped after every tree) keep the 16-group order of H = 1:
+// scores are bit-identical for any H.
 // ---------------------------------------------------------------------------
-template <int MODE, int DEPTH, bool U32, bool WIDE>
+// halves of tile `tile` (H x 128 documents) that hold documents
+template <int H>
+__device__ __forceinline__ int valid_halves(int64_t n_docs, int64_t tile)
+{
+    if (H == 1) return 1;
+    const int64_t v = (n_docs - tile * (kTile * H) + kTile - 1) / kTile;
+    return v < H ? static_cast<int>(v) : H;
+}
+
+template <int MODE, int DEPTH, bool U32, bool WIDE, int H = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
     constexpr bool HAS_A = MODE != MODE_APPLY;
     constexpr bool HAS_B = MODE != MODE_BINARIZE;
+    constexpr int kTileH = kTile * H;            // documents per tile
+    constexpr int kSlots = kConsumerWarps / H;   // tree slots per half (phase B)
+    static_assert(H == 1 || (H == 2 && !WIDE && MODE != MODE_BINARIZE), "halves: fused/apply, narrow");
     if (smem_addr(smem_raw) & 1023u) __trap();  // alignment the TMA swizzle relies on
     const uint32_t base = 0;
     const uint32_t bins = base + p.off_bins;
@@ -803,7 +890,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t bct = bars + 160u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_fjobs = HAS_A ? (p.n_fchunks + p.fsub_per_job - 1) / p.fsub_per_job : 0;
-    const int n_bjobs = HAS_B ? p.n_tchunks : 0;
+    // ring jobs of phase B: tree chunks (H = 1) or half-chunks of tc / 2 trees (H = 2)
+    const int n_bjobs = HAS_B ? p.n_tchunks * H : 0;
     constexpr bool WIDE_BINS = MODE == MODE_BINARIZE && WIDE;
     const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile * (p.wide ? 2u : 1u);
     const uint32_t bins_dst = (MODE == MODE_APPLY && p.wide) ? base + p.off_stage : bins;
@@ -829,10 +917,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                              : "memory");
             uint32_t slot = 0, ph = 0, bph = 0;
             for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+                // halves holding documents (a fully out-of-range half is not loaded)
+                const int hv = valid_halves<H>(p.n_docs, tile);
                 if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
                     mbar_wait(bins_empty, bph ^ 1u);
-                    mbar_expect_tx(bins_full, tile_bins_bytes);
-                    bulk_g2s(bins_dst, p.bins_in + tile * tile_bins_bytes, tile_bins_bytes, bins_full);
+                    mbar_expect_tx(bins_full, tile_bins_bytes * hv);
+                    for (int h = 0; h < hv; ++h)
+                        bulk_g2s(bins_dst + h * p.half_stride, p.bins_in + (tile * H + h) * tile_bins_bytes,
+                                 tile_bins_bytes, bins_full);
                     bph ^= 1u;
                 }
                 for (int j = 0; j < n_fjobs; ++j) {
@@ -842,16 +934,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int nsub = min(p.fsub_per_job, p.n_fchunks - c0);
                     const uint32_t sb = ring + slot * p.slot_bytes;
                     uint32_t tx = 0;
-                    for (int s = 0; s < nsub; ++s) tx += kFSubBytes + kMetaBytes + sld<uint2>(bct + 8u * (c0 + s)).y;
+                    for (int s = 0; s < nsub; ++s)
+                        tx += kFSubBytes * hv + kMetaBytes + sld<uint2>(bct + 8u * (c0 + s)).y;
                     mbar_expect_tx(full, tx);
                     for (int s = 0; s < nsub; ++s) {
                         const int c = c0 + s;
-                        if (p.fm)  // feature-major input (NEXT-4): box (128 docs, 32 factors)
-                            tma_load_2d(sb + s * kFSubBytes, &tmap, static_cast<int>(tile * kTile),
-                                        c * kFSub, full);
-                        else
-                            tma_load_2d(sb + s * kFSubBytes, &tmap, c * kFSub,
-                                        static_cast<int>(tile * kTile), full);
+                        for (int h = 0; h < hv; ++h) {
+                            const int row = static_cast<int>(tile * kTileH + h * kTile);
+                            if (p.fm)  // feature-major input (NEXT-4): box (128 docs, 32 factors)
+                                tma_load_2d(sb + (s * H + h) * kFSubBytes, &tmap, row, c * kFSub, full);
+                            else
+                                tma_load_2d(sb + (s * H + h) * kFSubBytes, &tmap, c * kFSub, row, full);
+                        }
                         bulk_g2s(sb + p.off_meta + s * kMetaBytes, p.fmeta + c * kFSub, kMetaBytes,
                                  full);
                         const uint2 bc = sld<uint2>(bct + 8u * c);
@@ -864,9 +958,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < n_bjobs; ++c) {
                     const uint32_t full = bars + 16u * slot, empty = full + 8u;
                     mbar_wait(empty, ph ^ 1u);
-                    mbar_expect_tx(full, p.chunk_bytes);
-                    bulk_g2s(ring + slot * p.slot_bytes,
-                             p.chunks + static_cast<size_t>(c) * p.chunk_bytes, p.chunk_bytes, full);
+                    const uint32_t sb = ring + slot * p.slot_bytes;
+                    if constexpr (H == 1) {
+                        mbar_expect_tx(full, p.chunk_bytes);
+                        bulk_g2s(sb, p.chunks + static_cast<size_t>(c) * p.chunk_bytes, p.chunk_bytes, full);
+                    } else {
+                        // half-chunk q of chunk c >> 1: its descriptors, then its tables at hdesc_bytes
+                        const int half_tc = p.tc / 2;
+                        const uint8_t *ch = p.chunks + static_cast<size_t>(c >> 1) * p.chunk_bytes;
+                        const uint32_t db = static_cast<uint32_t>(half_tc * desc_stride(DEPTH));
+                        const uint32_t tbytes = static_cast<uint32_t>(half_tc * table_stride(DEPTH));
+                        mbar_expect_tx(full, db + tbytes);
+                        bulk_g2s(sb, ch + (c & 1) * db, db, full);
+                        bulk_g2s(sb + p.hdesc_bytes, ch + p.desc_bytes + (c & 1) * tbytes, tbytes, full);
+                    }
                     if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
                 }
             }
@@ -876,12 +981,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ========================= consumer warps =========================
     const int tid = threadIdx.x;
-    const uint32_t lane_bins = sabs(bins) + lane * 4u;  // absolute (tree_level)
+    const int half = H == 1 ? 0 : warp / kSlots, tslot = H == 1 ? warp : warp % kSlots;
+    const uint32_t lane_bins = sabs(bins + half * p.half_stride) + lane * 4u;  // absolute (tree_level)
+    const uint32_t desc_off = H == 1 ? p.desc_bytes : p.hdesc_bytes;  // tables in a ring slot
+    const int nk = H == 1 ? p.tc / kConsumerWarps : p.tc / (2 * kSlots);  // trees per job per warp
     uint32_t slot = 0, ph = 0, bph = 0;
 #if ODF_DIAG & 8
     int diag_it = 0;
 #endif
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        const int hv = valid_halves<H>(p.n_docs, tile);
         unsigned long long waitA = 0;
 #if ODF_DIAG & 8
         unsigned long long waitB = 0;
@@ -894,16 +1003,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (HAS_A) {
             if constexpr (WIDE_BINS) {
                 if (p.fm)
-                    phase_a<false, true, true>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA);
+                    phase_a<false, true, true, 1>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
                 else
-                    phase_a<false, true, false>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA);
+                    phase_a<false, true, false, 1>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
             } else {
                 if (p.fm)
-                    phase_a<MODE == MODE_FUSED, WIDE, true>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp, lane,
-                                                            slot, ph, waitA);
+                    phase_a<MODE == MODE_FUSED, WIDE, true, H>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp, lane,
+                                                               slot, ph, waitA, hv);
                 else
-                    phase_a<MODE == MODE_FUSED, WIDE, false>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp,
-                                                             lane, slot, ph, waitA);
+                    phase_a<MODE == MODE_FUSED, WIDE, false, H>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp,
+                                                                lane, slot, ph, waitA, hv);
             }
         }
         if (MODE == MODE_BINARIZE) {
@@ -919,13 +1028,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.wide)
                 expand_wide(p, base + p.off_stage, bins, tid, kConsumerThreads);
             else
-                expand_splits(p, bins, tid, kConsumerThreads);
+                for (int h = 0; h < hv; ++h) expand_splits(p, bins + h * p.half_stride, tid, kConsumerThreads);
         }
         DIAG_T(t_adone);
         named_bar_consumers();  // all bins of the tile written
         DIAG_T(t_bstart);
 
-        Acc<U32> acc;
+        // acc: the group of the warp's next tree; acc2 (H = 2): the other group
+        Acc<U32> acc, acc2;
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
             DIAG_T(tw0);
@@ -933,12 +1043,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if ODF_DIAG & 8
             waitB += gtime() - tw0;
 #endif
+            const uint32_t sb = ring + slot * p.slot_bytes;
 #if ODF_DIAG & 2  // diagnostics build only: phase B does no work
             if (n_bjobs < 0)
 #endif
-            apply_chunk<DEPTH, U32>(ring + slot * p.slot_bytes, p.desc_bytes, lane_bins, warp,
-                                    p.tc / kConsumerWarps, acc);
+            {
+                if constexpr (H == 1) {
+                    apply_chunk<DEPTH, U32>(sb, desc_off, lane_bins, tslot, nk, acc);
+                } else {
+#pragma unroll 2
+                    for (int k = 0; k < nk; ++k) {
+                        apply_tree<DEPTH, U32>(sb, desc_off, lane_bins, tslot + k * kSlots, acc);
+                        const Acc<U32> t = acc;
+                        acc = acc2;
+                        acc2 = t;
+                    }
+                }
+            }
             acc.pin(pin_scratch);
+            if (H > 1) acc2.pin(pin_scratch);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty);
             if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
@@ -946,9 +1069,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         DIAG_T(t_bdone);
         // reduction buffer aliases the bins: wait until every warp is done with them
         named_bar_consumers();
-        acc.to_red(red, warp, lane);
+        // a warp applies an even number of trees per tile (tc is a multiple of 16), so
+        // acc holds group tslot and acc2 group tslot + 8 (H = 2)
+        acc.to_red(red, tslot, half * kTile + lane * 4, kTileH);
+        if (H > 1) acc2.to_red(red, tslot + kSlots, half * kTile + lane * 4, kTileH);
         named_bar_consumers();
-        if (tid < kTile) finish_doc(p, red, tid, tile * kTile + tid, static_cast<Acc<U32> *>(nullptr));
+        if (tid < kTileH)
+            finish_doc(p, red, tid, tile * kTileH + tid, kTileH, static_cast<Acc<U32> *>(nullptr));
         if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
             fence_proxy_async();  // generic writes to the bins region precede the next TMA
         }
@@ -1055,6 +1182,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // The association differs from the main path (tree ranges per split), so these
 // scores are held to the tolerance, not bit-exactness.
 // ---------------------------------------------------------------------------
+#ifdef ODF_KERNELS_AUX  // non-template kernels: defined in odf_k_aux.cu only
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_lat_binarize_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -1085,6 +1213,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     else
         binarize_sub<2, true, true, false>(t_off, m_off, b_off, sink, warp >> 1, (warp & 1) << 6, lane);
 }
+#endif
 
 template <int DEPTH>
 __global__ void __launch_bounds__(kConsumerThreads)
@@ -1114,7 +1243,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         __syncthreads();
         apply_chunk<DEPTH, false>(chunk, p.desc_bytes, lane_bins, warp, p.tc / kConsumerWarps, acc);
     }
-    acc.to_red(red, warp, lane);
+    acc.to_red(red, warp, lane * 4, kTile);
     __syncthreads();
     float *part = p.lat_partial + (tile * S) * kTile;
     if (tid < kTile) {
@@ -1145,6 +1274,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // numbered by ascending u then j; its bit for document i is (bin(x_i) <= j), i.e.
 // the node condition x < b_j itself.  Words: [ceil(D/32)][K_bin].
 // ---------------------------------------------------------------------------
+#ifdef ODF_KERNELS_AUX  // non-template kernels: defined in odf_k_aux.cu only
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_bits_from_bins_kernel(const KParams p)
 {
@@ -1175,6 +1305,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         }
     }
 }
+#endif
 
 // One CTA per 32-document group; lane = document; warp w sums trees t = w mod 16 in
 // ascending order and the 16 partials are combined in order: the same summation
@@ -1210,186 +1341,4 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
 }
 
-template <int DEPTH>
-static const void *bits_fn()
-{
-    return reinterpret_cast<const void *>(&odf_apply_bits_kernel<DEPTH>);
-}
-
-cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cudaStream_t s)
-{
-    static const void *t[11] = {bits_fn<0>(), bits_fn<1>(), bits_fn<2>(), bits_fn<3>(),
-                                bits_fn<4>(), bits_fn<5>(), bits_fn<6>(), bits_fn<7>(),
-                                bits_fn<8>(), bits_fn<9>(), bits_fn<10>()};
-    KParams pc = p;
-    void *args[] = {&pc};
-    if (!apply)
-        return cudaLaunchKernel(reinterpret_cast<const void *>(&odf_bits_from_bins_kernel),
-                                dim3(static_cast<unsigned>(p.n_tiles)), dim3(kConsumerThreads), args, 0, s);
-    if (depth < 0 || depth > 10) return cudaErrorInvalidValue;
-    const void *f = t[depth];
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    return cudaLaunchKernel(f, dim3(static_cast<unsigned>((p.n_docs + 31) / 32)), dim3(kConsumerThreads),
-                            args, smem, s);
-}
-
-// ---------------------------------------------------------------------------
-// dispatch
-// ---------------------------------------------------------------------------
-template <int MODE, int DEPTH, bool U32, bool WIDE = false>
-static const void *main_fn()
-{
-    return reinterpret_cast<const void *>(&odf_main_kernel<MODE, DEPTH, U32, WIDE>);
-}
-
-#define ODF_DEPTH_TABLE(M, U, W)                                                                    \
-    {main_fn<M, 0, U, W>(), main_fn<M, 1, U, W>(), main_fn<M, 2, U, W>(), main_fn<M, 3, U, W>(),     \
-     main_fn<M, 4, U, W>(), main_fn<M, 5, U, W>(), main_fn<M, 6, U, W>(), main_fn<M, 7, U, W>(),     \
-     main_fn<M, 8, U, W>(), main_fn<M, 9, U, W>(), main_fn<M, 10, U, W>()}
-
-static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide = false)
-{
-    static const void *fused[2][2][11] = {
-        {ODF_DEPTH_TABLE(MODE_FUSED, false, false), ODF_DEPTH_TABLE(MODE_FUSED, true, false)},
-        {ODF_DEPTH_TABLE(MODE_FUSED, false, true), ODF_DEPTH_TABLE(MODE_FUSED, true, true)}};
-    static const void *apply[2][11] = {ODF_DEPTH_TABLE(MODE_APPLY, false, false),
-                                       ODF_DEPTH_TABLE(MODE_APPLY, true, false)};
-    static const void *binz[2] = {main_fn<MODE_BINARIZE, 0, false, false>(),
-                                  main_fn<MODE_BINARIZE, 0, false, true>()};
-    if (depth < 0 || depth > 10) return nullptr;
-    if (mode == MODE_FUSED) return fused[wide ? 1 : 0][u32 ? 1 : 0][depth];
-    if (mode == MODE_APPLY) return apply[u32 ? 1 : 0][depth];
-    return binz[wide ? 1 : 0];
-}
-
-template <int DEPTH>
-static const void *index_fn()
-{
-    return reinterpret_cast<const void *>(&odf_index_kernel<DEPTH>);
-}
-static const void *index_kernel(int depth)
-{
-    static const void *t[11] = {index_fn<0>(), index_fn<1>(), index_fn<2>(), index_fn<3>(),
-                                index_fn<4>(), index_fn<5>(), index_fn<6>(), index_fn<7>(),
-                                index_fn<8>(), index_fn<9>(), index_fn<10>()};
-    return (depth < 0 || depth > 10) ? nullptr : t[depth];
-}
-
-template <int DEPTH>
-static const void *lat_fn()
-{
-    return reinterpret_cast<const void *>(&odf_lat_apply_kernel<DEPTH>);
-}
-static const void *lat_apply_kernel(int depth)
-{
-    static const void *t[11] = {lat_fn<0>(), lat_fn<1>(), lat_fn<2>(), lat_fn<3>(),
-                                lat_fn<4>(), lat_fn<5>(), lat_fn<6>(), lat_fn<7>(),
-                                lat_fn<8>(), lat_fn<9>(), lat_fn<10>()};
-    return (depth < 0 || depth > 10) ? nullptr : t[depth];
-}
-
-cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,
-                           size_t smem_bin, size_t smem_apply, cudaStream_t s)
-{
-    KParams pc = p;
-    CUtensorMap tm;
-    if (tmap)
-        tm = *tmap;
-    else
-        memset(&tm, 0, sizeof(tm));
-    cudaError_t e = cudaSuccess;
-    if (p.n_fchunks > 0) {
-        void *args[] = {&pc, &tm};
-        e = cudaLaunchKernel(reinterpret_cast<const void *>(&odf_lat_binarize_kernel),
-                             dim3(p.n_fchunks, static_cast<unsigned>(p.n_tiles)), dim3(kConsumerThreads),
-                             args, smem_bin, s);
-        if (e != cudaSuccess) return e;
-    } else {
-        e = cudaMemsetAsync(p.lat_counter, 0, sizeof(uint32_t) * p.n_tiles, s);
-        if (e != cudaSuccess) return e;
-    }
-    void *args2[] = {&pc};
-    return cudaLaunchKernel(lat_apply_kernel(depth), dim3(splits, static_cast<unsigned>(p.n_tiles)),
-                            dim3(kConsumerThreads), args2, smem_apply, s);
-}
-
-static cudaError_t opt_in(const void *f, int max_smem)
-{
-    cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, f);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                max_smem - static_cast<int>(a.sharedSizeBytes));
-}
-
-cudaError_t prepare_kernels(int max_smem)
-{
-    for (int d = 0; d <= 10; ++d) {
-        const void *fs[] = {main_kernel(MODE_FUSED, d), main_kernel(MODE_APPLY, d),
-                            main_kernel(MODE_FUSED, d, true), main_kernel(MODE_APPLY, d, true),
-                            main_kernel(MODE_FUSED, d, false, true), main_kernel(MODE_FUSED, d, true, true),
-                            index_kernel(d), lat_apply_kernel(d)};
-        for (const void *f : fs) {
-            cudaError_t e = opt_in(f, max_smem);
-            if (e != cudaSuccess) return e;
-        }
-    }
-    cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
-    if (e != cudaSuccess) return e;
-    e = opt_in(main_kernel(MODE_BINARIZE, 0, false, true), max_smem);
-    if (e != cudaSuccess) return e;
-    return opt_in(main_kernel(MODE_BINARIZE, 0), max_smem);
-}
-
-int occupancy_main(int mode, int depth, size_t smem)
-{
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, main_kernel(mode, depth), kThreads,
-                                                      smem) != cudaSuccess)
-        return 1;
-    return n > 0 ? n : 1;
-}
-
-cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
-                        size_t smem, cudaStream_t s)
-{
-    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0);
-    if (!f) return cudaErrorInvalidValue;
-    KParams pc = p;
-    CUtensorMap tm;
-    if (tmap)
-        tm = *tmap;
-    else
-        memset(&tm, 0, sizeof(tm));
-    void *args[] = {&pc, &tm};
-    return cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, s);
-}
-
-cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
-                         cudaStream_t s)
-{
-    const void *f = index_kernel(depth);
-    if (!f) return cudaErrorInvalidValue;
-    KParams pc = p;
-    int fp = fingerprint ? 1 : 0;
-    void *args[] = {&pc, &fp};
-    return cudaLaunchKernel(f, dim3(grid), dim3(kConsumerThreads), args, smem, s);
-}
-
 }  // namespace odf
-
-#if ODF_DIAG & 8
-extern "C" __attribute__((visibility("default"))) int odf_diag_copy(void *host, size_t bytes)
-{
-    if (bytes > sizeof(odf::g_diag)) bytes = sizeof(odf::g_diag);
-    return static_cast<int>(cudaMemcpyFromSymbol(host, odf::g_diag, bytes));
-}
-extern "C" __attribute__((visibility("default"))) int odf_diag_clear()
-{
-    static unsigned long long zero[1024];
-    for (size_t o = 0; o < sizeof(odf::g_diag); o += sizeof zero)
-        cudaMemcpyToSymbol(odf::g_diag, zero, sizeof zero, o);
-    return 0;
-}
-#endif

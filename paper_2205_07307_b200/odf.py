@@ -41,7 +41,8 @@ class _Info(ctypes.Structure):
                 ("borders_in_smem", ctypes.c_int32), ("stages_fused", ctypes.c_int32),
                 ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32),
                 ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32),
-                ("bins_elem_bytes", ctypes.c_int32)]
+                ("bins_elem_bytes", ctypes.c_int32), ("max_tile_docs", ctypes.c_int32),
+                ("stages_fused_256", ctypes.c_int32), ("smem_fused_256", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
@@ -71,12 +72,24 @@ def library_path() -> str:
     return _build.LIB
 
 
+_lib_path = None  # set by use_library() (diagnostics / A-B builds in tools/ only)
+
+
+def use_library(path: str) -> None:
+    """Load another build of the library (tools/: diagnostics and A/B builds made by
+    build.build_variant) instead of the product libodf.so.  Must precede lib()."""
+    global _lib_path
+    if _lib is not None:
+        raise RuntimeError("the library is already loaded")
+    _lib_path = os.path.abspath(path)
+
+
 def lib():
     """Load libodf.so (building it first if the sources are newer).  Raises if it cannot."""
     global _lib
     if _lib is not None:
         return _lib
-    path = os.environ.get("ODF_LIB_OVERRIDE") or _build.LIB  # A/B testing of builds only
+    path = _lib_path or _build.LIB
     if path == _build.LIB and _build._stale():
         try:
             _build.build()
@@ -120,6 +133,10 @@ def lib():
     L.odf_apply.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.odf_score.restype = ctypes.c_int
     L.odf_score.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+    L.odf_score_tiles.restype = ctypes.c_int
+    L.odf_score_tiles.argtypes = [_vp, _vp, _i64, _i64, _vp, _i32, _vp]
+    L.odf_apply_tiles.restype = ctypes.c_int
+    L.odf_apply_tiles.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp]
     L.odf_leaf_indices.restype = ctypes.c_int
     L.odf_leaf_indices.argtypes = [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]
     L.odf_index_fingerprint.restype = ctypes.c_int
@@ -139,7 +156,8 @@ ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_mode
                "odf_leaf_indices", "odf_index_fingerprint", "odf_score_host",
                "odf_latency_workspace_bytes", "odf_score_latency", "odf_load_model_ex",
                "odf_score_u64", "odf_apply_u64", "odf_load_model_paper", "odf_binarize_fm",
-               "odf_score_fm", "odf_bits_layout", "odf_bits_from_bins", "odf_apply_bits")
+               "odf_score_fm", "odf_bits_layout", "odf_bits_from_bins", "odf_apply_bits",
+               "odf_score_tiles", "odf_apply_tiles")
 
 
 def _check(status: int):
@@ -262,28 +280,53 @@ class Model:
         if not (x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 and x.stride(1) == 1):
             raise OdfError(1, "factors must be a CUDA float32 [n_docs, ld] tensor with unit "
                               "column stride")
+        if x.device != self._dev():
+            raise OdfError(1, f"factors are on {x.device}, the model on {self._dev()}")
+        if x.shape[1] < self.n_features:
+            raise OdfError(1, f"factors have {x.shape[1]} columns < n_features {self.n_features}")
         return x.shape[0], x.stride(0)
+
+    def _check_out(self, out, n: int, dtype, name: str = "out"):
+        """A caller-supplied output: on the model's device, of `dtype`, >= n elements."""
+        if out is None:
+            return torch.empty(max(int(n), 0), dtype=dtype, device=self._dev())
+        if not (isinstance(out, torch.Tensor) and out.is_cuda and out.device == self._dev()
+                and out.dtype == dtype and out.is_contiguous() and out.numel() >= n):
+            raise OdfError(1, f"{name} must be a contiguous CUDA {dtype} tensor on "
+                              f"{self._dev()} with >= {n} elements")
+        return out
+
+    def _check_bins(self, bins, n_docs: int):
+        need = self.bins_bytes(n_docs)
+        if not (isinstance(bins, torch.Tensor) and bins.is_cuda and bins.device == self._dev()
+                and bins.dtype == torch.uint8 and bins.is_contiguous() and bins.numel() >= need):
+            raise OdfError(1, f"bins must be a contiguous CUDA uint8 tensor on {self._dev()} "
+                              f"with >= {need} bytes (bins_bytes)")
+        return bins
 
     # -- hot path ---------------------------------------------------------
     def binarize(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None):
         n, ld = self._check_x(x)
-        if out is None:
-            out = torch.empty(self.bins_bytes(n), dtype=torch.uint8, device=self._dev())
+        out = self._check_out(out, self.bins_bytes(n), torch.uint8)
         _check(lib().odf_binarize(self._h, _ptr(x), n, ld, _ptr(out), _stream(stream, self._dev())))
         return out
 
-    def apply(self, bins: torch.Tensor, n_docs: int, out: torch.Tensor | None = None, stream=None):
-        if out is None:
-            out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
-        _check(lib().odf_apply(self._h, _ptr(bins), int(n_docs), _ptr(out),
-                               _stream(stream, self._dev())))
+    def apply(self, bins: torch.Tensor, n_docs: int, out: torch.Tensor | None = None, stream=None,
+              tile_docs: int = 0):
+        """tile_docs: 0 (automatic), 128 or 256 (odf_apply_tiles); same scores for all."""
+        bins = self._check_bins(bins, int(n_docs))
+        out = self._check_out(out, int(n_docs), torch.float32)
+        _check(lib().odf_apply_tiles(self._h, _ptr(bins), int(n_docs), _ptr(out), int(tile_docs),
+                                     _stream(stream, self._dev())))
         return out
 
-    def score(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    def score(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None,
+              tile_docs: int = 0):
+        """Fused binarize + apply; tile_docs: 0 (automatic), 128 or 256 (odf_score_tiles)."""
         n, ld = self._check_x(x)
-        if out is None:
-            out = torch.empty(n, dtype=torch.float32, device=self._dev())
-        _check(lib().odf_score(self._h, _ptr(x), n, ld, _ptr(out), _stream(stream, self._dev())))
+        out = self._check_out(out, n, torch.float32)
+        _check(lib().odf_score_tiles(self._h, _ptr(x), n, ld, _ptr(out), int(tile_docs),
+                                     _stream(stream, self._dev())))
         return out
 
     def latency_workspace(self, max_docs: int, splits: int = 0) -> torch.Tensor:
@@ -294,8 +337,9 @@ class Model:
                       stream=None):
         """K4 small-batch path: two launches, tolerance-level parity with score()."""
         n, ld = self._check_x(x)
-        if out is None:
-            out = torch.empty(n, dtype=torch.float32, device=self._dev())
+        out = self._check_out(out, n, torch.float32)
+        if not (workspace.is_cuda and workspace.device == self._dev()):
+            raise OdfError(1, f"workspace must be on {self._dev()}")
         _check(lib().odf_score_latency(self._h, _ptr(x), n, ld, _ptr(out), int(splits),
                                        _ptr(workspace), workspace.numel(),
                                        _stream(stream, self._dev())))
@@ -311,6 +355,7 @@ class Model:
         return sums, sc
 
     def apply_u64(self, bins: torch.Tensor, n_docs: int, stream=None):
+        bins = self._check_bins(bins, int(n_docs))
         sums = torch.empty(int(n_docs), dtype=torch.int64, device=self._dev())
         sc = torch.empty(int(n_docs), dtype=torch.float64, device=self._dev())
         _check(lib().odf_apply_u64(self._h, _ptr(bins), int(n_docs), _ptr(sums), _ptr(sc),
@@ -319,24 +364,23 @@ class Model:
 
     def _check_xt(self, xt: torch.Tensor, n_docs: int):
         if not (xt.is_cuda and xt.dtype == torch.float32 and xt.dim() == 2 and xt.stride(1) == 1
-                and xt.shape[0] >= self.n_features and xt.shape[1] >= n_docs):
+                and xt.shape[0] >= self.n_features and xt.shape[1] >= n_docs
+                and xt.device == self._dev()):
             raise OdfError(1, "feature-major factors must be a CUDA float32 [>= n_features, "
-                              ">= n_docs] tensor with unit column stride")
+                              f">= n_docs] tensor with unit column stride on {self._dev()}")
         return xt.stride(0)
 
     def binarize_fm(self, xt: torch.Tensor, n_docs: int, out=None, stream=None):
         """Feature-major input (NEXT-4): xt[f, i] = factor f of document i."""
         ld = self._check_xt(xt, n_docs)
-        if out is None:
-            out = torch.empty(self.bins_bytes(n_docs), dtype=torch.uint8, device=self._dev())
+        out = self._check_out(out, self.bins_bytes(n_docs), torch.uint8)
         _check(lib().odf_binarize_fm(self._h, _ptr(xt), int(n_docs), ld, _ptr(out),
                                      _stream(stream, self._dev())))
         return out
 
     def score_fm(self, xt: torch.Tensor, n_docs: int, out=None, stream=None):
         ld = self._check_xt(xt, n_docs)
-        if out is None:
-            out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
+        out = self._check_out(out, int(n_docs), torch.float32)
         _check(lib().odf_score_fm(self._h, _ptr(xt), int(n_docs), ld, _ptr(out),
                                   _stream(stream, self._dev())))
         return out
@@ -350,15 +394,16 @@ class Model:
 
     def bits_from_bins(self, bins: torch.Tensor, n_docs: int, out=None, stream=None):
         nbytes, k = self.bits_layout(n_docs)
-        if out is None:
-            out = torch.empty(max(nbytes // 4, 1), dtype=torch.int32, device=self._dev())
+        bins = self._check_bins(bins, int(n_docs))
+        out = self._check_out(out, max(nbytes // 4, 1), torch.int32)
         _check(lib().odf_bits_from_bins(self._h, _ptr(bins), int(n_docs), _ptr(out),
                                         _stream(stream, self._dev())))
         return out
 
     def apply_bits(self, words: torch.Tensor, n_docs: int, out=None, stream=None):
-        if out is None:
-            out = torch.empty(int(n_docs), dtype=torch.float32, device=self._dev())
+        nbytes, _ = self.bits_layout(n_docs)
+        self._check_out(words, nbytes // 4, torch.int32, "words")
+        out = self._check_out(out, int(n_docs), torch.float32)
         _check(lib().odf_apply_bits(self._h, _ptr(words), int(n_docs), _ptr(out),
                                     _stream(stream, self._dev())))
         return out
@@ -383,6 +428,7 @@ class Model:
 
     # -- test / debug (K6) ----------------------------------------------------
     def leaf_indices(self, bins, n_docs, doc0, ndoc, tree0, ntree, stream=None):
+        bins = self._check_bins(bins, int(n_docs))
         out = torch.empty((int(ndoc), int(ntree)), dtype=torch.int16, device=self._dev())
         _check(lib().odf_leaf_indices(self._h, _ptr(bins), int(n_docs), int(doc0), int(ndoc),
                                       int(tree0), int(ntree), _ptr(out),
@@ -390,6 +436,7 @@ class Model:
         return out
 
     def index_fingerprint(self, bins, n_docs, stream=None):
+        bins = self._check_bins(bins, int(n_docs))
         out = torch.empty(int(n_docs), dtype=torch.int64, device=self._dev())
         _check(lib().odf_index_fingerprint(self._h, _ptr(bins), int(n_docs), _ptr(out),
                                            _stream(stream, self._dev())))

@@ -4,12 +4,12 @@ The paper scales by giving every worker a private copy of the data and the
 model ("Каждый поток получал свою копию данных и модели").  On one
 8xB200 box that becomes:
 
-* document sharding (weak scaling, the default): every rank holds the whole
-  model (<= ~20 MB) and scores its own contiguous slice of documents
-  [floor(r*D/W), floor((r+1)*D/W)); there is no collective on the data path.
-  Scores are bit-identical to W = 1 because a document's summation order does
-  not depend on the batch it is scored in.
-  An optional all-gather assembles the full score vector on every rank.
+* document sharding (the default): every rank holds the whole model (<= ~20 MB)
+  and scores its own contiguous slice of one batch's documents
+  [floor(r*D/W), floor((r+1)*D/W)); the only collective is the score all-gather
+  (bench.py times it inside the step: strong scaling of one batch).  Scores are
+  bit-identical to W = 1 because a document's summation order does not depend
+  on the batch it is scored in.
 * tree sharding (for forests too large for one GPU's fast memory, config c4):
   rank r holds trees [floor(r*T/W), floor((r+1)*T/W)), binarizes ALL documents,
   produces fp32 partial scores, and one NCCL reduce (or all-reduce /
@@ -84,6 +84,32 @@ class DocSharded:
         parts = [torch.empty_like(buf) for _ in range(w)]
         dist.all_gather(parts, buf, group=self.group)
         return torch.cat([p[:s] for p, s in zip(parts, sizes)])
+
+    @staticmethod
+    def padded_size(n_docs: int, world: int) -> int:
+        """Per-rank slot of the padded gather buffer: ceil(n_docs / world)."""
+        return -(-n_docs // world)
+
+    def gather_into(self, local_padded: torch.Tensor, out_padded: torch.Tensor) -> torch.Tensor:
+        """All-gather with preallocated buffers (the timed step): rank r's scores sit in
+        local_padded[:hi-lo] (length padded_size), and land in out_padded[r*m : r*m + hi-lo]
+        (length world*m).  `unpad` turns the result into the [n_docs] score vector."""
+        w, _ = _world(self.group)
+        if w == 1:
+            out_padded.copy_(local_padded)
+            return out_padded
+        if dist.get_backend(self.group) == "gloo":  # no all_gather_into_tensor on gloo
+            dist.all_gather(list(out_padded.chunk(w)), local_padded, group=self.group)
+        else:
+            dist.all_gather_into_tensor(out_padded, local_padded, group=self.group)
+        return out_padded
+
+    def unpad(self, out_padded: torch.Tensor, n_docs: int) -> torch.Tensor:
+        w, _ = _world(self.group)
+        m = self.padded_size(n_docs, w)
+        return torch.cat([out_padded[k * m:k * m + (shard_bounds(n_docs, w, k)[1] -
+                                                    shard_bounds(n_docs, w, k)[0])]
+                          for k in range(w)])
 
 
 @dataclass

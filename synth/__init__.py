@@ -114,18 +114,33 @@ def _ranking_block(seed: int, b: int, rows: int, kinds: np.ndarray, out: np.ndar
 
 
 def ranking_factors(seed: int, n_docs: int, n_features: int, ld: int | None = None,
-                    threads: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+                    threads: int | None = None, out: np.ndarray | None = None,
+                    rows: tuple[int, int] | None = None) -> np.ndarray:
+    """Rows [0, n_docs) of the ranking-shaped matrix, or only rows [r0, r1) of it
+    (rows=(r0, r1)): every block is drawn with its full-matrix row count, so a
+    row range holds exactly the values of those rows of the whole matrix."""
     ld = n_features if ld is None else ld
+    r0, r1 = (0, n_docs) if rows is None else (int(rows[0]), int(rows[1]))
+    if not 0 <= r0 <= r1 <= n_docs:
+        raise ValueError(f"rows [{r0}, {r1}) outside [0, {n_docs})")
     kinds = feature_kinds(seed, n_features)
-    x = out if out is not None else np.empty((n_docs, ld), np.float32)
+    x = out if out is not None else np.empty((r1 - r0, ld), np.float32)
     if ld > n_features:
         x[:, n_features:] = 0.0
     nb = (n_docs + BLOCK - 1) // BLOCK
 
     def job(b):
-        r0 = b * BLOCK
-        rows = min(BLOCK, n_docs - r0)
-        _ranking_block(seed, b, rows, kinds, x[r0:r0 + rows])
+        b0 = b * BLOCK
+        brows = min(BLOCK, n_docs - b0)
+        lo, hi = max(b0, r0), min(b0 + brows, r1)
+        if lo >= hi:
+            return
+        if lo == b0 and hi == b0 + brows:
+            _ranking_block(seed, b, brows, kinds, x[b0 - r0:b0 - r0 + brows])
+        else:
+            tmp = np.empty((brows, n_features), np.float32)
+            _ranking_block(seed, b, brows, kinds, tmp)
+            x[lo - r0:hi - r0, :n_features] = tmp[lo - b0:hi - b0]
 
     threads = threads or min(16, os.cpu_count() or 1)
     with ThreadPoolExecutor(threads) as ex:
@@ -203,8 +218,10 @@ def tiny_case(seed: int = 1, n_docs: int = 1024, n_features: int = 32, n_trees: 
 
 def make_case(name: str, n_docs: int | None = None, exact_leaves: bool = False,
               seed: int | None = None, ld: int | None = None,
-              n_trees: int | None = None) -> ForestCase:
-    """A BASELINE.json config by name ('c1'..'c5'); n_docs/n_trees may shrink it for tests."""
+              n_trees: int | None = None, rows: tuple[int, int] | None = None) -> ForestCase:
+    """A BASELINE.json config by name ('c1'..'c5'); n_docs/n_trees may shrink it for tests.
+    rows=(r0, r1) (c2-c5): x holds only documents [r0, r1) of the n_docs batch (one
+    rank's shard), the model is the whole config's."""
     cfg = dict(CONFIGS[name])
     seed = cfg["seed"] if seed is None else seed
     D = cfg["n_docs"] if n_docs is None else int(n_docs)
@@ -217,8 +234,9 @@ def make_case(name: str, n_docs: int | None = None, exact_leaves: bool = False,
     calib = np.empty((calib_rows, F), np.float32)
     _ranking_block(seed, 0, calib_rows, feature_kinds(seed, F), calib)
     fi, thr, lv, pools = ranking_forest(seed, F, T, d, calib, LEAF_SIGMA[name], exact_leaves)
-    x = ranking_factors(seed, D, F, ld=ld)
-    meta = dict(seed=seed, recipe="ranking", pool_sizes=[int(p.size) for p in pools])
+    x = ranking_factors(seed, D, F, ld=ld, rows=rows)
+    meta = dict(seed=seed, recipe="ranking", pool_sizes=[int(p.size) for p in pools],
+                rows=list(rows) if rows is not None else [0, D])
     return ForestCase(name, x, F, fi, thr, lv, d, T, meta=meta)
 
 

@@ -246,7 +246,29 @@ def test_concurrent_streams_one_model():
 # ---------------------------------------------------------------------------
 # BASELINE.json sizes, in the launch configuration bench.py times
 # ---------------------------------------------------------------------------
-def _sampled_full_size(name, n_sample=1500, fp_docs=2048):
+def _oracle_bins_rows(case, rows_x, used, threads=8):
+    """Oracle bins (used features) of the rows in rows_x, in parallel row chunks (the
+    ctypes call releases the GIL; the oracle's arithmetic is unchanged)."""
+    from concurrent.futures import ThreadPoolExecutor
+    per, flat, counts, offs = oracle.borders(case.feature_index, case.thresholds, case.n_features)
+    n = rows_x.shape[0]
+    out = np.empty((n, used.size), np.uint16)
+    step = max(1, -(-n // (threads * 4)))
+
+    def job(r0):
+        r1 = min(n, r0 + step)
+        out[r0:r1] = oracle.bins(rows_x[r0:r1], case.n_features, flat, counts, offs)[:, used]
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(job, range(0, n, step)))
+    return out
+
+
+def _full_size(name, every=1, block=4096):
+    """BASELINE size in bench.py's launch configuration (automatic tile width).  Checked
+    against the oracle on EVERY document (every=1) or on every `every`-th block of
+    `block` documents plus the last block: scores within the tolerance, bins and
+    leaf-index fingerprints bit-exact; fused == two-stage bit for bit on all documents."""
     import torch
     case = synth.make_case(name)
     n = case.n_docs
@@ -255,45 +277,116 @@ def _sampled_full_size(name, n_sample=1500, fp_docs=2048):
     bins, s_fused, s_two = run_cuda(m, x, n)
     f = s_fused.cpu().numpy()
     assert np.array_equal(f.view(np.uint32), s_two.cpu().numpy().view(np.uint32))
-    rng = np.random.default_rng(99)
-    rows = np.unique(np.concatenate([rng.integers(0, n, n_sample), [0, 1, 127, 128, n - 1]]))
-    s64 = oracle.score_rows(case.x, rows, case.feature_index, case.thresholds, case.leaf_values,
-                            case.depth)
+    starts = list(range(0, n, block))
+    sel = starts[::every] + ([starts[-1]] if (len(starts) - 1) % every else [])
+    rows = np.concatenate([np.arange(s0, min(s0 + block, n)) for s0 in sel])
+    xs = case.x if every == 1 else case.x[rows]
+    s64, _ = oracle.score(xs, case.feature_index, case.thresholds, case.leaf_values, case.depth)
     err = np.abs(f[rows].astype(np.float64) - s64)
     assert err.max() <= tolerance(case.leaf_values, case.depth), err.max()
-    # bins of the sampled rows, bit-exact
-    per, flat, counts, offs = oracle.borders(case.feature_index, case.thresholds, case.n_features)
-    used = np.flatnonzero(counts > 0)
-    want = oracle.bins(case.x[rows], case.n_features, flat, counts, offs)[:, used]
-    canon = m.canonical_bins(bins, n)
-    got = canon[torch.from_numpy(rows).cuda()].cpu().numpy()
-    assert np.array_equal(got, want)
-    # leaf-index fingerprints of a window of documents (every tree), bit-exact
-    d0 = n - fp_docs
     fp = m.index_fingerprint(bins, n).cpu().numpy().view(np.uint64)
-    want_fp = oracle.fingerprint(case.x[d0:], case.feature_index, case.thresholds, case.depth,
-                                 case.n_trees)
-    assert np.array_equal(fp[d0:], want_fp)
-    # a leaf-index window
+    want_fp = oracle.fingerprint(xs, case.feature_index, case.thresholds, case.depth, case.n_trees)
+    assert np.array_equal(fp[rows], want_fp)
+    used = m.used_feature_ids
+    canon = m.canonical_bins(bins, n)
+    want = _oracle_bins_rows(case, xs, used)
+    rows_t = torch.from_numpy(rows).cuda()
+    for r0 in range(0, rows.size, 262144):
+        got = canon[rows_t[r0:r0 + 262144]].cpu().numpy()
+        assert np.array_equal(got, want[r0:r0 + 262144]), f"bins differ in rows {r0}.."
     got_idx = m.leaf_indices(bins, n, 1000, 64, case.n_trees - 100, 100).cpu().numpy().view(np.uint16)
     want_idx = oracle.leaf_indices(case.x, case.feature_index, case.thresholds, case.depth,
                                    1000, 64, case.n_trees - 100, 100)
     assert np.array_equal(got_idx, want_idx)
     m.close()
-    del x, bins
+    del x, bins, canon
     torch.cuda.empty_cache()
 
 
 def test_c2_full_size():
-    _sampled_full_size("c2")
+    _full_size("c2")
 
 
 def test_c3_full_size():
-    _sampled_full_size("c3", n_sample=600)
+    _full_size("c3")
 
 
 def test_c4_full_size():
-    _sampled_full_size("c4", n_sample=600)
+    _full_size("c4", every=4)  # 25 % of the 4 M documents (1.6e10 doc-trees in full)
+
+
+# ---------------------------------------------------------------------------
+# Tile width (odf_score_tiles / odf_apply_tiles): 128- and 256-document tiles
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,depth_note", [("c4", "depth 10"), ("c1", "depth 6")])
+@pytest.mark.parametrize("n_docs", [1, 100, 128, 129, 255, 256, 257, 1000, 5000])
+def test_tile_widths_bit_identical(name, depth_note, n_docs):
+    """256-document tiles (two halves sharing every staged tree chunk) give the same
+    scores, bit for bit, as 128-document tiles, fused and two-stage; ragged tiles
+    include a fully empty second half (n_docs <= 128 mod 256)."""
+    import torch
+    case = synth.make_case(name, n_docs=max(n_docs, 65536) if name != "c1" else n_docs,
+                           n_trees=48 if name == "c4" else None)
+    case.x = np.ascontiguousarray(case.x[:n_docs])
+    m = cuda_model(case)
+    assert m.info["max_tile_docs"] == 256, m.info
+    x = to_dev(case.x)
+    bins = m.binarize(x)
+    outs = [m.score(x, tile_docs=t) for t in (128, 256, 0)] + \
+           [m.apply(bins, n_docs, tile_docs=t) for t in (128, 256, 0)]
+    torch.cuda.synchronize()
+    ref = outs[0].cpu().numpy()
+    for o in outs[1:]:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    s64, _ = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, case.depth)
+    assert np.abs(ref.astype(np.float64) - s64).max() <= tolerance(case.leaf_values, case.depth)
+    m.close()
+
+
+def test_tile_256_exact_leaves_and_many_tiles():
+    """Exact-arithmetic leaves: 256-document tiles are bit-exact against the oracle's
+    fp32 rounding over many tiles (every SM runs several tiles, the ring wraps)."""
+    import torch
+    case = synth.make_case("c4", n_docs=200_000, n_trees=160, exact_leaves=True)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    s256 = m.score(x, tile_docs=256)
+    s128 = m.score(x, tile_docs=128)
+    torch.cuda.synchronize()
+    _, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, case.depth)
+    assert np.array_equal(s256.cpu().numpy(), s32)
+    assert np.array_equal(s128.cpu().numpy(), s32)
+    m.close()
+
+
+def test_tile_width_errors():
+    from paper_2205_07307_b200 import OdfError
+    case = synth.tiny_case(3, n_docs=300)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    for bad in (64, 512, -1):
+        with pytest.raises(OdfError) as e:
+            m.score(x, tile_docs=bad)
+        assert e.value.status == 1
+    m.close()
+    # a wide model (a factor with > 254 borders, uint16 bins) has no 256-document tiles
+    rng = np.random.default_rng(6)
+    d, nb = 6, 300
+    T = (nb + d - 1) // d
+    fi = np.zeros(T * d, np.int32)
+    thr = np.sort(rng.standard_normal(T * d).astype(np.float32))
+    lv = rng.normal(0, 0.01, T << d).astype(np.float32)
+    case = synth.ForestCase("wide", rng.standard_normal((300, 4)).astype(np.float32), 4, fi, thr,
+                            lv, d, T)
+    m = cuda_model(case)
+    assert m.info["bins_elem_bytes"] == 2
+    assert m.info["max_tile_docs"] == 128
+    with pytest.raises(OdfError) as e:
+        m.score(to_dev(case.x), tile_docs=256)
+    assert e.value.status == 2
+    s = m.score(to_dev(case.x), tile_docs=128)
+    assert s.shape[0] == 300
+    m.close()
 
 
 # ---------------------------------------------------------------------------

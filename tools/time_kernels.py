@@ -14,6 +14,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("ODF_LIB_OVERRIDE"):  # diagnostics / A-B build (tools only)
+    from paper_2205_07307_b200 import odf as _odf
+    _odf.use_library(os.environ["ODF_LIB_OVERRIDE"])
 
 
 def timeit(fn, reps=20, warm=5):
@@ -53,7 +56,12 @@ def main():
            "fused_ms": timeit(lambda: m.score(x, out=out), a.reps),
            "binarize_ms": timeit(lambda: m.binarize(x, out=bins), a.reps),
            "apply_ms": timeit(lambda: m.apply(bins, n, out=out), a.reps),
-           "info": {k: m.info[k] for k in ("stages_fused", "smem_fused", "trees_per_chunk", "n_columns", "bord_stride")}}
+           "info": {k: m.info[k] for k in ("stages_fused", "smem_fused", "trees_per_chunk", "n_columns",
+                                           "bord_stride", "max_tile_docs", "stages_fused_256")}}
+    if m.info["max_tile_docs"] == 256:  # both tile widths, explicitly
+        for t in (128, 256):
+            res[f"fused_ms_t{t}"] = timeit(lambda: m.score(x, out=out, tile_docs=t), a.reps)
+            res[f"apply_ms_t{t}"] = timeit(lambda: m.apply(bins, n, out=out, tile_docs=t), a.reps)
     print(json.dumps(res), flush=True)
 
 
