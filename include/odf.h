@@ -266,7 +266,10 @@ ODF_API odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bi
  * (about 2 CTAs per SM).  d_workspace: device memory of at least
  * odf_latency_workspace_bytes(m, n_docs, splits) bytes (same `splits`), owned by
  * the caller; concurrent calls need distinct workspaces.  Same argument rules as
- * odf_score.  Capturable in a CUDA graph.                                      */
+ * odf_score, and n_docs <= 65535 x 128 (ODF_E_INVALID_ARG above: tiles are a grid
+ * dimension; this is the small-batch path).  Capturable in a CUDA graph (two
+ * kernel nodes; the factor pointer is baked into the captured tensor map, so a
+ * graph serves one input buffer, tests/test_gpu_parity.py::test_latency_graph). */
 ODF_API size_t odf_latency_workspace_bytes(const odf_model *m, int64_t n_docs, int32_t splits);
 ODF_API odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t n_docs,
                                      int64_t ld, float *d_scores, int32_t splits,

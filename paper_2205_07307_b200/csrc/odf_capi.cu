@@ -11,7 +11,8 @@
 //  * 7-bit code columns: column A of f holds min(bin,127); factors with
 //    m_f > 127 also get column B = max(bin-127, 0); a node tests
 //    "code >= K" on column A with K = k+1 when k+1 <= 127, else on column B
-//    with K = k-126;  level descriptor = (col << 19) | (128-K)  (odf_internal.h);
+//    with K = k-126;  level descriptor {col * 128, (128-K) * 0x01010101} for depth
+//    <= 8, (col << 19) | (128-K) for depth 9-10  (odf_internal.h desc_stride);
 //  * leaf tables reversed (table[F] = leaf[2^d-1-F]) because the kernels
 //    assemble the complemented index F (flags are "condition false"), and
 //    bank-swizzled (leaf_pos: words sharing a shared-memory bank are far apart
@@ -332,6 +333,22 @@ int choose_halves(const odf_model *m, int mode, int64_t n_docs, int32_t tile_doc
 // ============================================================================
 // ABI
 // ============================================================================
+// No exception crosses the ABI (include/odf.h): host allocations of the model
+// compiler and the staging of odf_score_host are the only sources.
+template <class F>
+static odf_status guarded(F f)
+{
+    try {
+        return f();
+    } catch (const std::bad_alloc &) {
+        return fail(ODF_E_NOMEM, "host allocation failed");
+    } catch (const std::exception &e) {
+        return fail(ODF_E_INVALID_ARG, "unexpected host exception: %s", e.what());
+    } catch (...) {
+        return fail(ODF_E_INVALID_ARG, "unexpected host exception");
+    }
+}
+
 extern "C" {
 
 int odf_version(void) { return 100; }
@@ -383,7 +400,9 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
     return odf_load_model_ex(&d, out);
 }
 
-odf_status odf_load_model_paper(const odf_paper_model_desc *d, odf_model **out)
+static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out);
+
+static odf_status load_model_paper_impl(const odf_paper_model_desc *d, odf_model **out)
 {
     if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
@@ -412,6 +431,10 @@ odf_status odf_load_model_paper(const odf_paper_model_desc *d, odf_model **out)
         n_cond += static_cast<int64_t>(h) * d->stc[h];
         n_leaf += (int64_t(1) << h) * d->stc[h];
     }
+    if (T > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
+    if ((T << D) > (int64_t(1) << 32))  // checked before the host arrays are allocated
+        return fail(ODF_E_UNSUPPORTED, "%lld trees x 2^%d replicated answers > 2^32",
+                    (long long)T, D);
     if (n_cond > 0 && !d->cond_indices) return fail(ODF_E_INVALID_ARG, "cond_indices is NULL");
     if (n_leaf > 0 && !d->leaves) return fail(ODF_E_INVALID_ARG, "leaves is NULL");
     std::vector<int32_t> fi(static_cast<size_t>(T) * D);
@@ -460,10 +483,10 @@ odf_status odf_load_model_paper(const odf_paper_model_desc *d, odf_model **out)
     md.device = d->device;
     md.scale = d->scale;
     md.bias = d->bias;
-    return odf_load_model_ex(&md, out);
+    return load_model_ex_impl(&md, out);
 }
 
-odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
+static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out)
 {
     if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
@@ -503,10 +526,9 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
             if (!std::isfinite(leaf_f[k]))
                 return fail(ODF_E_INVALID_ARG, "leaf_values[%lld] is not finite", (long long)k);
 
-    int n_dev = 0;
-    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
-        return fail(ODF_E_CUDA, "no CUDA device available (this library has no CPU fallback)");
-    if (device < 0 || device >= n_dev) return fail(ODF_E_INVALID_ARG, "device %d not in [0, %d)", device, n_dev);
+    if (n_leaves > (int64_t(1) << 32))
+        return fail(ODF_E_UNSUPPORTED, "%lld answers > 2^32", (long long)n_leaves);
+    if (device < 0) return fail(ODF_E_INVALID_ARG, "device %d < 0", device);
 
     std::unique_ptr<odf_model> m(new odf_model());
     m->device = device;
@@ -646,6 +668,9 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
     m->desc_bytes = align_up(static_cast<uint64_t>(m->tc) * dstride, 256);
     m->chunk_bytes = m->desc_bytes + static_cast<uint32_t>(m->tc) * m->table_stride;
     m->n_tchunks = static_cast<int32_t>((n_trees + m->tc - 1) / m->tc);
+    if (static_cast<int64_t>(m->n_tchunks) * m->chunk_bytes > (int64_t(1) << 36))
+        return fail(ODF_E_NOMEM, "tree chunks of %lld bytes > 64 GiB",
+                    (long long)(static_cast<int64_t>(m->n_tchunks) * m->chunk_bytes));
     std::vector<uint8_t> chunks(static_cast<size_t>(m->n_tchunks) * m->chunk_bytes, 0);
     // padding trees of the last chunk: -0.0 answers (x + -0.0 == x bit for bit) / 0
     if (!u32 && n_trees % m->tc != 0) {
@@ -671,7 +696,7 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
             const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
                                         : static_cast<uint32_t>(colB_of[f]) + c - 1u;
             const uint32_t K = k - 127u * c + 1u;
-            if (ODF_DESC8) {
+            if (desc8(depth)) {
                 desc[2 * l] = col * kTile;
                 desc[2 * l + 1] = (128u - K) * 0x01010101u;
             } else {
@@ -706,7 +731,12 @@ odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
         }
     }
 
-    // ---- device ----
+    // ---- device (the host-side compile above needs none: it runs, and is
+    //      sanitizer-checked, on CPU-only hosts too, tests/test_sanitizers.py) ----
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+        return fail(ODF_E_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    if (device >= n_dev) return fail(ODF_E_INVALID_ARG, "device %d not in [0, %d)", device, n_dev);
     int prev = 0;
     cudaGetDevice(&prev);
     cudaError_t e = cudaSetDevice(device);
@@ -1106,6 +1136,8 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    if ((n_docs + kTile - 1) / kTile > 65535)  // tiles are the grid's y dimension
+        return fail(ODF_E_INVALID_ARG, "latency path: n_docs > 65535 x 128 (use odf_score)");
     const int sp = lat_splits(m, n_docs, splits);
     size_t off[4];
     lat_layout(m, n_docs, sp, off);
@@ -1144,12 +1176,15 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     return ok();
 }
 
-odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,
-                          float *h_scores, int64_t chunk_docs, void *stream)
+static odf_status score_host_impl(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,
+                                  float *h_scores, int64_t chunk_docs, void *stream)
 {
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "odf_score_host: fp32-leaf models only");
     if (n_docs < 0 || ld < m->n_features || ld % 4 != 0)
         return fail(ODF_E_INVALID_ARG, "bad n_docs / ld (ld >= n_features, ld %% 4 == 0)");
+    if (n_docs >= (int64_t(1) << 31) - kTile)
+        return fail(ODF_E_INVALID_ARG, "n_docs >= 2^31 - 128 (TMA coordinate range)");
     if (n_docs == 0) return ok();
     if (!h_factors || !h_scores) return fail(ODF_E_INVALID_ARG, "NULL host buffer");
     if (chunk_docs <= 0) chunk_docs = 65536;
@@ -1183,6 +1218,13 @@ odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, 
     cudaEventRecord(m->ev_in, us);
     cudaStreamWaitEvent(m->hs[0], m->ev_in, 0);
     cudaStreamWaitEvent(m->hs[1], m->ev_in, 0);
+    // on an error after work was queued: wait for both staging streams, so no copy
+    // from or to the caller's host buffers is still running when the call returns
+    auto drain = [&](odf_status st) {
+        cudaStreamSynchronize(m->hs[0]);
+        cudaStreamSynchronize(m->hs[1]);
+        return st;
+    };
     int64_t k = 0;
     for (int64_t d0 = 0; d0 < n_docs; d0 += chunk_docs, ++k) {
         const int b = static_cast<int>(k & 1);
@@ -1190,13 +1232,12 @@ odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, 
         cudaStream_t s = m->hs[b];
         if ((e = cudaMemcpyAsync(m->d_stage[b], h_factors + d0 * ld, static_cast<size_t>(n) * ld * 4,
                                  cudaMemcpyHostToDevice, s)) != cudaSuccess)
-            return cuda_fail(e, "H2D");
-        if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "odf_score_host: fp32-leaf models only");
+            return drain(cuda_fail(e, "H2D"));
         odf_status st = odf_score(m, m->d_stage[b], n, ld, m->d_sstage[b], s);
-        if (st != ODF_OK) return st;
+        if (st != ODF_OK) return drain(st);
         if ((e = cudaMemcpyAsync(h_scores + d0, m->d_sstage[b], static_cast<size_t>(n) * 4,
                                  cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-            return cuda_fail(e, "D2H");
+            return drain(cuda_fail(e, "D2H"));
     }
     for (int i = 0; i < 2; ++i) {
         cudaEventRecord(m->ev_out[i], m->hs[i]);
@@ -1204,6 +1245,22 @@ odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, 
     }
     if ((e = cudaStreamSynchronize(us)) != cudaSuccess) return cuda_fail(e, "odf_score_host");
     return ok();
+}
+
+odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out)
+{
+    return guarded([&] { return load_model_ex_impl(desc, out); });
+}
+
+odf_status odf_load_model_paper(const odf_paper_model_desc *d, odf_model **out)
+{
+    return guarded([&] { return load_model_paper_impl(d, out); });
+}
+
+odf_status odf_score_host(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,
+                          float *h_scores, int64_t chunk_docs, void *stream)
+{
+    return guarded([&] { return score_host_impl(m, h_factors, n_docs, ld, h_scores, chunk_docs, stream); });
 }
 
 }  // extern "C"

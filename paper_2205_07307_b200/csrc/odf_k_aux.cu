@@ -94,9 +94,20 @@ cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap,
         e = cudaMemsetAsync(p.lat_counter, 0, sizeof(uint32_t) * p.n_tiles, s);
         if (e != cudaSuccess) return e;
     }
+    // kernel (2) with programmatic stream serialization after kernel (1): it launches
+    // while (1) runs, stages its first chunk and waits (griddepcontrol.wait) for (1)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(splits, static_cast<unsigned>(p.n_tiles));
+    cfg.blockDim = dim3(kConsumerThreads);
+    cfg.dynamicSmemBytes = smem_apply;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = p.n_fchunks > 0 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     void *args2[] = {&pc};
-    return cudaLaunchKernel(lat_apply_kernel(depth), dim3(splits, static_cast<unsigned>(p.n_tiles)),
-                            dim3(kConsumerThreads), args2, smem_apply, s);
+    return cudaLaunchKernelExC(&cfg, lat_apply_kernel(depth), args2);
 }
 
 static cudaError_t opt_in(const void *f, int max_smem)

@@ -506,11 +506,22 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
 // and leaf tables are stored reversed (table[F] = leaf[2^d-1-F]).
 // Descriptors are 4 bytes per level (odf_internal.h): 6 levels cost one LDS.128
 // and one LDS.64 broadcast instead of three LDS.128.
+// A lane's view of a tile's code block: the absolute address of its 4 documents'
+// bytes in code column 0.
+struct Lane {
+    uint32_t bins;
+};
+__device__ __forceinline__ Lane make_lane(const KParams &, uint32_t bins_abs) { return Lane{bins_abs}; }
+// One level: the lane's code word of the level's column, and the byte-wise
+// "code >= K" flags in bit 7 (code + (128 - K) never carries out of its byte),
+// shifted into the index.  (Moving the address / merge onto the FMA pipe with
+// IMAD.HI was tried: SASS IMAD.HI takes a 64-bit addend, so every merge needs a
+// register-pair set-up and the FMA pipe became the binder.)
 template <int DEPTH>
-__device__ __forceinline__ void tree_level(uint32_t dsc, uint32_t lane_bins, int l, uint32_t &lo,
+__device__ __forceinline__ void tree_level(uint32_t dsc, const Lane &ln, int l, uint32_t &lo,
                                            uint32_t &hi)
 {
-    const uint32_t w = ldsa_u32(lane_bins + (dsc >> 12));  // col * 128; absolute address
+    const uint32_t w = ldsa_u32(ln.bins + (dsc >> 12));  // col * 128; absolute address
     const uint32_t s = (w + prmt(dsc, 0u, 0x0000u)) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
@@ -518,12 +529,12 @@ __device__ __forceinline__ void tree_level(uint32_t dsc, uint32_t lane_bins, int
         hi = (l == 8) ? s : ((hi >> 1) | s);
 }
 
-// 8-byte descriptors (ODF_DESC8): {col * 128, (128 - K) replicated in every byte}
+// 8-byte descriptors (depth <= 8): {col * 128, (128 - K) replicated in every byte}
 template <int DEPTH>
-__device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, uint32_t lane_bins, int l,
+__device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, const Lane &ln, int l,
                                             uint32_t &lo, uint32_t &hi)
 {
-    const uint32_t w = ldsa_u32(lane_bins + col128);
+    const uint32_t w = ldsa_u32(ln.bins + col128);
     const uint32_t s = (w + krep) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
@@ -532,44 +543,44 @@ __device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, uint
 }
 
 template <int DEPTH>
-__device__ __forceinline__ void tree_flags(uint32_t d, uint32_t lane_bins, uint32_t &lo,
+__device__ __forceinline__ void tree_flags(uint32_t d, const Lane &ln, uint32_t &lo,
                                            uint32_t &hi)
 {
     lo = 0;
     hi = 0;
-#if ODF_DESC8
+    if constexpr (desc8(DEPTH)) {
 #pragma unroll
-    for (int l = 0; l < DEPTH; l += 2) {  // one LDS.128 per two levels
-        const uint4 q = lds_v4u(d + l * 8);
-        tree_level8<DEPTH>(q.x, q.y, lane_bins, l, lo, hi);
-        if (l + 1 < DEPTH) tree_level8<DEPTH>(q.z, q.w, lane_bins, l + 1, lo, hi);
-    }
-#else
+        for (int l = 0; l < DEPTH; l += 2) {  // one LDS.128 per two levels
+            const uint4 q = lds_v4u(d + l * 8);
+            tree_level8<DEPTH>(q.x, q.y, ln, l, lo, hi);
+            if (l + 1 < DEPTH) tree_level8<DEPTH>(q.z, q.w, ln, l + 1, lo, hi);
+        }
+    } else {
 #pragma unroll
     for (int l = 0; l < DEPTH; l += 4) {
         if (l + 2 < DEPTH) {  // 3 or 4 levels left: one LDS.128 (padding levels unused)
             const uint4 q = lds_v4u(d + l * 4);
-            tree_level<DEPTH>(q.x, lane_bins, l, lo, hi);
-            tree_level<DEPTH>(q.y, lane_bins, l + 1, lo, hi);
-            tree_level<DEPTH>(q.z, lane_bins, l + 2, lo, hi);
-            if (l + 3 < DEPTH) tree_level<DEPTH>(q.w, lane_bins, l + 3, lo, hi);
+            tree_level<DEPTH>(q.x, ln, l, lo, hi);
+            tree_level<DEPTH>(q.y, ln, l + 1, lo, hi);
+            tree_level<DEPTH>(q.z, ln, l + 2, lo, hi);
+            if (l + 3 < DEPTH) tree_level<DEPTH>(q.w, ln, l + 3, lo, hi);
         } else if (l + 1 < DEPTH) {
             const uint2 q = lds_v2u(d + l * 4);
-            tree_level<DEPTH>(q.x, lane_bins, l, lo, hi);
-            tree_level<DEPTH>(q.y, lane_bins, l + 1, lo, hi);
+            tree_level<DEPTH>(q.x, ln, l, lo, hi);
+            tree_level<DEPTH>(q.y, ln, l + 1, lo, hi);
         } else {
-            tree_level<DEPTH>(lds_u32(d + l * 4), lane_bins, l, lo, hi);
+            tree_level<DEPTH>(lds_u32(d + l * 4), ln, l, lo, hi);
         }
     }
-#endif
+    }
 }
 
 // Complemented leaf index F of the lane's 4 documents.
 template <int DEPTH>
-__device__ __forceinline__ void tree_findex(uint32_t d, uint32_t lane_bins, uint32_t F[4])
+__device__ __forceinline__ void tree_findex(uint32_t d, const Lane &ln, uint32_t F[4])
 {
     uint32_t lo, hi;
-    tree_flags<DEPTH>(d, lane_bins, lo, hi);
+    tree_flags<DEPTH>(d, ln, lo, hi);
 #pragma unroll
     for (int n = 0; n < 4; ++n) {
         if constexpr (DEPTH == 0) {
@@ -606,11 +617,11 @@ __device__ __forceinline__ uint32_t swz_bank_hi(uint32_t lo, uint32_t h)
 // Absolute shared-window addresses of the 4 leaves (tables reversed and
 // bank-swizzled; tb = the table base, absolute and 256-aligned).
 template <int DEPTH>
-__device__ __forceinline__ void leaf_addrs(uint32_t d, uint32_t lane_bins, uint32_t tb,
+__device__ __forceinline__ void leaf_addrs(uint32_t d, const Lane &ln, uint32_t tb,
                                            uint32_t a[4])
 {
     uint32_t lo, hi;
-    tree_flags<DEPTH>(d, lane_bins, lo, hi);
+    tree_flags<DEPTH>(d, ln, lo, hi);
     if constexpr (DEPTH <= 6) {
         // byte = F << (8-DEPTH); want 4F in the low byte of a 256-aligned base
         if constexpr (DEPTH < 6 && DEPTH > 0) lo >>= (6 - DEPTH);
@@ -704,10 +715,13 @@ struct Acc<true> {
 #ifndef ODF_APPLY_UNROLL
 #define ODF_APPLY_UNROLL 2
 #endif
+#ifndef ODF_UNROLL3
+#define ODF_UNROLL3 0  // 3 trees per iteration when a warp's trees per chunk are a multiple of 3 (A/B)
+#endif
 constexpr int kApplyUnroll = ODF_APPLY_UNROLL;  // trees in flight per warp
 
 template <int DEPTH, bool U32>
-__device__ __forceinline__ void apply_tree(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
+__device__ __forceinline__ void apply_tree(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
                                            int i, Acc<U32> &acc)
 {
     const uint32_t d = chunk + i * desc_stride(DEPTH);
@@ -715,22 +729,27 @@ __device__ __forceinline__ void apply_tree(uint32_t chunk, uint32_t desc_bytes, 
     // leaf_addrs yields absolute leaf addresses with no base add
     const uint32_t tb = sabs(chunk + desc_bytes + i * table_stride(DEPTH));
     uint32_t a[4];
-    leaf_addrs<DEPTH>(d, lane_bins, tb, a);
+    leaf_addrs<DEPTH>(d, ln, tb, a);
     acc.add4(a);
 }
 
 template <int DEPTH, bool U32>
-__device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, uint32_t lane_bins,
+__device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
                                             int warp, int nk, Acc<U32> &acc)
 {
     // chunks hold nk * 16 trees (the last one padded with zero-answer trees); a
     // multiple of 4 trees per warp runs 4 trees per iteration (warp-uniform choice)
     if (DEPTH <= 6 && (nk & 3) == 0) {
 #pragma unroll 4
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, lane_bins, warp + k * kConsumerWarps, acc);
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+#if ODF_UNROLL3
+    } else if (DEPTH <= 6 && nk % 3 == 0) {  // e.g. c3: 96-tree chunks, 6 trees per warp
+#pragma unroll 3
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+#endif
     } else {
 #pragma unroll kApplyUnroll
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, lane_bins, warp + k * kConsumerWarps, acc);
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
     }
 }
 
@@ -982,7 +1001,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ========================= consumer warps =========================
     const int tid = threadIdx.x;
     const int half = H == 1 ? 0 : warp / kSlots, tslot = H == 1 ? warp : warp % kSlots;
-    const uint32_t lane_bins = sabs(bins + half * p.half_stride) + lane * 4u;  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * 4u);  // absolute (tree_level)
     const uint32_t desc_off = H == 1 ? p.desc_bytes : p.hdesc_bytes;  // tables in a ring slot
     const int nk = H == 1 ? p.tc / kConsumerWarps : p.tc / (2 * kSlots);  // trees per job per warp
     uint32_t slot = 0, ph = 0, bph = 0;
@@ -1049,11 +1068,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             {
                 if constexpr (H == 1) {
-                    apply_chunk<DEPTH, U32>(sb, desc_off, lane_bins, tslot, nk, acc);
+                    apply_chunk<DEPTH, U32>(sb, desc_off, ln, tslot, nk, acc);
                 } else {
 #pragma unroll 2
                     for (int k = 0; k < nk; ++k) {
-                        apply_tree<DEPTH, U32>(sb, desc_off, lane_bins, tslot + k * kSlots, acc);
+                        apply_tree<DEPTH, U32>(sb, desc_off, ln, tslot + k * kSlots, acc);
                         const Acc<U32> t = acc;
                         acc = acc2;
                         acc2 = t;
@@ -1120,7 +1139,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             expand_splits(p, bins, tid, kConsumerThreads);
         __syncthreads();
     }
-    const uint32_t lane_bins = sabs(bins) + lane * 4u;  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins) + lane * 4u);  // absolute (tree_level)
     const int64_t t_lo = fingerprint ? 0 : p.tree0;
     const int64_t t_hi = fingerprint ? p.n_trees : p.tree0 + p.ntree;
     uint64_t h[4] = {0xcbf29ce484222325ull, 0xcbf29ce484222325ull, 0xcbf29ce484222325ull,
@@ -1136,7 +1155,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             if (warp == 0) {
                 for (int i = 0; i < p.tc && c0 + i < p.n_trees; ++i) {
                     uint32_t F[4];
-                    tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), lane_bins, F);
+                    tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), ln, F);
 #pragma unroll
                     for (int n = 0; n < 4; ++n) {
                         const uint32_t idx = F[n] ^ ((1u << DEPTH) - 1u);
@@ -1150,7 +1169,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
                 const int64_t t = c0 + i;
                 if (t < p.tree0 || t >= t_hi) continue;
                 uint32_t F[4];
-                tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), lane_bins, F);
+                tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), ln, F);
 #pragma unroll
                 for (int n = 0; n < 4; ++n) {
                     const int64_t doc = tile * kTile + lane * 4 + n;
@@ -1205,6 +1224,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (bc.y) bulk_g2s(b_off, reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, bar);
         if (c == 0) p.lat_counter[tile] = 0u;  // ticket for kernel (2), stream-ordered
     }
+    // programmatic dependent launch: kernel (2) may start now (it stages its first
+    // tree chunk, then waits for this grid with griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
     mbar_wait(bar, 0);
     const GmemSink sink{p.lat_codes + tile * p.code_stride};
@@ -1227,21 +1249,30 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const uint32_t cols_bytes = static_cast<uint32_t>(p.n_cols) * kTile;
     const uint32_t chunk = (cols_bytes + 1023u) & ~1023u;
     const uint32_t red = chunk + ((p.chunk_bytes + 1023u) & ~1023u);
+    const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
+    const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
+    auto stage_chunk = [&](int c) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.chunks + static_cast<size_t>(c) * p.chunk_bytes);
+        for (uint32_t k = tid; k < p.chunk_bytes / 16; k += kConsumerThreads)
+            sts_v4u(chunk + 16 * k, __ldg(src + k));
+    };
+    // the first tree chunk does not depend on kernel (1): stage it before waiting for
+    // that grid (programmatic dependent launch; a plain launch makes the wait a no-op)
+    if (c_lo < c_hi) stage_chunk(c_lo);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(p.lat_codes + tile * p.code_stride);
         for (uint32_t k = tid; k < cols_bytes / 16; k += kConsumerThreads) sts_v4u(bins + 16 * k, src[k]);
     }
-    const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
-    const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
     Acc<false> acc;
-    const uint32_t lane_bins = sabs(bins) + lane * 4u;  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins) + lane * 4u);  // absolute (tree_level)
     for (int c = c_lo; c < c_hi; ++c) {
-        __syncthreads();  // previous chunk consumed (and, first time, codes stored)
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.chunks + static_cast<size_t>(c) * p.chunk_bytes);
-        for (uint32_t k = tid; k < p.chunk_bytes / 16; k += kConsumerThreads)
-            sts_v4u(chunk + 16 * k, __ldg(src + k));
-        __syncthreads();
-        apply_chunk<DEPTH, false>(chunk, p.desc_bytes, lane_bins, warp, p.tc / kConsumerWarps, acc);
+        if (c != c_lo) {
+            __syncthreads();  // previous chunk consumed
+            stage_chunk(c);
+        }
+        __syncthreads();  // chunk (and, first time, codes) stored
+        apply_chunk<DEPTH, false>(chunk, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
     }
     acc.to_red(red, warp, lane * 4, kTile);
     __syncthreads();

@@ -439,6 +439,61 @@ def test_latency_path_depth10_and_small_workspace_error():
 # ---------------------------------------------------------------------------
 # NEXT-1: MatrixNet integer leaves (u32 answers, u64 sums, (R - 2^31) S + B), zero tolerance
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("batch", [100, 1000, 5000])
+def test_latency_graph(batch):
+    """The K4 latency path captured in a CUDA graph (binarize kernel + apply kernel
+    with a programmatic dependent launch) replays bit-identically to direct calls on
+    the same input buffer, whatever that buffer holds, within the tolerance of the
+    oracle; replays reuse the captured workspace and tensor map."""
+    import torch
+    case = synth.make_case("c5", n_docs=65536, n_trees=1000)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    buf = x[:batch].clone()
+    ws = m.latency_workspace(batch)
+    out = torch.empty(batch, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up outside the capture
+        m.score_latency(buf, ws, out=out)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        m.score_latency(buf, ws, out=out)
+    tol = tolerance(case.leaf_values, case.depth)
+    for q, off in enumerate([0, 7000, 65536 - batch]):
+        buf.copy_(x[off:off + batch])
+        g.replay()
+        torch.cuda.synchronize()
+        got = out.clone()
+        ws2 = m.latency_workspace(batch)
+        direct = m.score_latency(buf, ws2)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int32), direct.view(torch.int32)), q
+        rows = np.arange(off, off + batch)[:: max(1, batch // 200)]
+        s64 = oracle.score_rows(case.x, rows, case.feature_index, case.thresholds,
+                                case.leaf_values, case.depth)
+        assert np.abs(got.cpu().numpy()[rows - off].astype(np.float64) - s64).max() <= tol
+    m.close()
+
+
+def test_latency_path_rejects_too_many_tiles():
+    from paper_2205_07307_b200 import OdfError
+    case = synth.tiny_case(2, n_docs=128)
+    m = cuda_model(case)
+    big = 65535 * 128 + 1
+    x = torch_empty_cuda((big, case.n_features))
+    with pytest.raises(OdfError) as e:
+        m.score_latency(x, m.latency_workspace(128))
+    assert e.value.status == 1
+    m.close()
+
+
+def torch_empty_cuda(shape):
+    import torch
+    return torch.empty(shape, dtype=torch.float32, device="cuda")
+
+
 @pytest.mark.parametrize("depth,n_docs,n_trees", [(6, 1000, 300), (3, 129, 1000), (10, 257, 40),
                                                   (0, 50, 7)])
 def test_integer_leaves_exact(depth, n_docs, n_trees):
