@@ -116,13 +116,17 @@ ODF_API odf_status odf_load_model_ex(const odf_model_desc *desc, odf_model **out
  * group's binary features are consecutive), one threshold per binary
  * feature, STC[h] = number of trees of height h (0..8), per-tree condition
  * indices into the binary features with trees stored in descending height
- * (P:307), u32 answers, and S, B of P:309.  The import builds a uniform-depth
- * integer model of depth D = the largest height present: a tree of height h < D
- * keeps its h conditions as levels 0..h-1, repeats its level 0 on levels h..D-1,
- * and its table is replicated (answer j = answer[j mod 2^h]), so those levels
- * cannot change its answer (height-0 trees: constant answer).  Score with
- * odf_score_u64 / odf_apply_u64 (exact).  Errors: ODF_E_INVALID_ARG for
- * out-of-range indices, heights > ODF_MAX_DEPTH, non-finite thresholds, sizes. */
+ * (P:307), u32 answers, and S, B of P:309.  The import keeps the paper's height
+ * mix: one segment per height present (descending, as stored), each staged and
+ * applied by the kernels at its own depth (a tree of height h costs h levels and a
+ * 2^h-entry table; the u64 sum is exact, so the order is free).  pad_heights = 1
+ * selects the earlier padded form instead: a uniform-depth model of depth D = the
+ * largest height, a tree of height h < D repeating its level 0 on levels h..D-1
+ * with its table replicated (answer j = answer[j mod 2^h]).  Both give the same
+ * sums.  Score with odf_score_u64 / odf_apply_u64 (exact); odf_leaf_indices /
+ * odf_index_fingerprint need a uniform-depth model (ODF_E_UNSUPPORTED for a
+ * mixed one).  Errors: ODF_E_INVALID_ARG for out-of-range indices, heights >
+ * ODF_MAX_DEPTH, non-finite thresholds, sizes.                                  */
 typedef struct {
     int32_t n_features;
     const int32_t *group_factor; /* [n_groups] */
@@ -134,6 +138,7 @@ typedef struct {
     const uint32_t *leaves;      /* [sum_h 2^h * stc[h]] */
     double scale, bias;
     int32_t device;
+    int32_t pad_heights;         /* 0: one segment per height (default); 1: padded uniform form */
 } odf_paper_model_desc;
 ODF_API odf_status odf_load_model_paper(const odf_paper_model_desc *desc, odf_model **out);
 

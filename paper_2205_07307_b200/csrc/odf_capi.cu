@@ -98,6 +98,9 @@ std::once_flag g_encode_once;
 struct odf_model {
     int device = 0, num_sms = 0, max_smem = 0;
     int32_t depth = 0, n_features = 0;
+    int32_t kdepth = 0;  // kernel instantiation: depth, or kMixedDepth for mixed-height models
+    int32_t n_seg = 0;   // mixed-height models (NEXT-2): height segments of the chunk stream
+    SegP seg[kMaxSegments] = {};
     int64_t n_trees = 0;
     std::vector<int32_t> used_ids;
     int32_t n_used = 0, n_split = 0, n_cols = 0;
@@ -267,6 +270,8 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.off_meta = pl.off_meta;
     p.off_bord = pl.off_bord;
     p.bord_stride = m->bord_stride;
+    p.n_seg = m->n_seg;
+    for (int sg = 0; sg < m->n_seg; ++sg) p.seg[sg] = m->seg[sg];
     p.half_stride = pl.half_stride;
     p.hdesc_bytes = pl.hdesc_bytes;
     return p;
@@ -400,7 +405,21 @@ odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
     return odf_load_model_ex(&d, out);
 }
 
-static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out);
+// One height segment of a model: n_trees trees of one depth (feature_index /
+// thresholds [n_trees * depth], answers [n_trees << depth]).
+struct SegSpec {
+    int32_t depth;
+    int64_t n_trees;
+    const int32_t *fi;
+    const float *thr;
+    const void *leaves;
+};
+static odf_status load_model_core(const odf_model_desc *desc, const std::vector<SegSpec> *segs_in,
+                                  odf_model **out);
+static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out)
+{
+    return load_model_core(desc, nullptr, out);
+}
 
 static odf_status load_model_paper_impl(const odf_paper_model_desc *d, odf_model **out)
 {
@@ -432,11 +451,55 @@ static odf_status load_model_paper_impl(const odf_paper_model_desc *d, odf_model
         n_leaf += (int64_t(1) << h) * d->stc[h];
     }
     if (T > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
-    if ((T << D) > (int64_t(1) << 32))  // checked before the host arrays are allocated
-        return fail(ODF_E_UNSUPPORTED, "%lld trees x 2^%d replicated answers > 2^32",
-                    (long long)T, D);
+    if ((d->pad_heights ? (T << D) : n_leaf) > (int64_t(1) << 32))  // before any host allocation
+        return fail(ODF_E_UNSUPPORTED, "%lld answers > 2^32",
+                    (long long)(d->pad_heights ? (T << D) : n_leaf));
     if (n_cond > 0 && !d->cond_indices) return fail(ODF_E_INVALID_ARG, "cond_indices is NULL");
     if (n_leaf > 0 && !d->leaves) return fail(ODF_E_INVALID_ARG, "leaves is NULL");
+    for (int64_t k = 0; k < n_cond; ++k)
+        if (d->cond_indices[k] >= static_cast<uint64_t>(K))
+            return fail(ODF_E_INVALID_ARG, "cond_indices[%lld] = %u >= K = %lld", (long long)k,
+                        d->cond_indices[k], (long long)K);
+    odf_model_desc md;
+    memset(&md, 0, sizeof md);
+    md.leaf_type = ODF_LEAF_U32;
+    md.n_features = d->n_features;
+    md.device = d->device;
+    md.scale = d->scale;
+    md.bias = d->bias;
+    if (!d->pad_heights) {
+        // one segment per height present, in the paper's order (descending height,
+        // P:307): tree t of height h keeps its h conditions and its 2^h answers
+        std::vector<std::vector<int32_t>> fis;
+        std::vector<std::vector<float>> thrs;
+        std::vector<std::vector<uint32_t>> lvs;
+        std::vector<SegSpec> segs;
+        int64_t cb = 0, lb = 0;
+        for (int h = ODF_MAX_DEPTH; h >= 0; --h) {
+            if (d->stc[h] == 0) continue;
+            const int64_t nt = d->stc[h];
+            fis.emplace_back(static_cast<size_t>(nt) * h);
+            thrs.emplace_back(static_cast<size_t>(nt) * h);
+            lvs.emplace_back(static_cast<size_t>(nt) << h);
+            for (int64_t k = 0; k < nt * h; ++k) {
+                const uint32_t ci = d->cond_indices[cb + k];
+                fis.back()[k] = bf_factor[ci];
+                thrs.back()[k] = d->thresholds[ci];
+            }
+            std::memcpy(lvs.back().data(), d->leaves + lb, sizeof(uint32_t) * (static_cast<size_t>(nt) << h));
+            cb += nt * h;
+            lb += nt << h;
+        }
+        int64_t k = 0;
+        for (int h = ODF_MAX_DEPTH; h >= 0; --h)
+            if (d->stc[h] > 0) {
+                segs.push_back(SegSpec{h, d->stc[h], fis[k].data(), thrs[k].data(), lvs[k].data()});
+                ++k;
+            }
+        if (segs.empty()) segs.push_back(SegSpec{0, 0, nullptr, nullptr, nullptr});
+        return load_model_core(&md, &segs, out);
+    }
+    // padded form (pad_heights = 1): a uniform model of depth D = the largest height
     std::vector<int32_t> fi(static_cast<size_t>(T) * D);
     std::vector<float> thr(static_cast<size_t>(T) * D);
     std::vector<uint32_t> lv(static_cast<size_t>(T) << D);
@@ -444,10 +507,9 @@ static odf_status load_model_paper_impl(const odf_paper_model_desc *d, odf_model
     int32_t f0 = 0;
     float th0 = 0.0f;
     if (n_cond > 0) {
-        const uint32_t k = d->cond_indices[0];
-        if (k >= static_cast<uint64_t>(K)) return fail(ODF_E_INVALID_ARG, "cond_indices[0] >= K");
-        f0 = bf_factor[k];
-        th0 = d->thresholds[k];
+        const uint32_t k0 = d->cond_indices[0];
+        f0 = bf_factor[k0];
+        th0 = d->thresholds[k0];
     }
     int64_t t = 0, cb = 0, lb = 0;
     for (int h = ODF_MAX_DEPTH; h >= 0; --h)  // "trees in descending height"
@@ -457,9 +519,6 @@ static odf_status load_model_paper_impl(const odf_paper_model_desc *d, odf_model
                 float th = th0;
                 if (h > 0) {
                     const uint32_t k = d->cond_indices[cb + (l < h ? l : 0)];
-                    if (k >= static_cast<uint64_t>(K))
-                        return fail(ODF_E_INVALID_ARG, "cond_indices[%lld] = %u >= K = %lld",
-                                    (long long)(cb + l), k, (long long)K);
                     f = bf_factor[k];
                     th = d->thresholds[k];
                 }
@@ -471,68 +530,78 @@ static odf_status load_model_paper_impl(const odf_paper_model_desc *d, odf_model
             cb += h;
             lb += int64_t(1) << h;
         }
-    odf_model_desc md;
-    memset(&md, 0, sizeof md);
     md.feature_index = fi.data();
     md.thresholds = thr.data();
     md.leaf_values = lv.data();
-    md.leaf_type = ODF_LEAF_U32;
     md.depth = D;
     md.n_trees = T;
-    md.n_features = d->n_features;
-    md.device = d->device;
-    md.scale = d->scale;
-    md.bias = d->bias;
     return load_model_ex_impl(&md, out);
 }
 
-static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out)
+// The model compiler (K0).  segs_in == nullptr: one uniform-depth segment from desc;
+// else the height segments of a mixed-height model (NEXT-2), in stream order.
+static odf_status load_model_core(const odf_model_desc *desc, const std::vector<SegSpec> *segs_in,
+                                  odf_model **out)
 {
     if (!out) return fail(ODF_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (!desc) return fail(ODF_E_INVALID_ARG, "desc is NULL");
-    const int32_t *feature_index = desc->feature_index;
-    const float *thresholds = desc->thresholds;
-    const int32_t depth = desc->depth;
-    const int64_t n_trees = desc->n_trees;
+    std::vector<SegSpec> segs;
+    if (segs_in)
+        segs = *segs_in;
+    else
+        segs.push_back(SegSpec{desc->depth, desc->n_trees, desc->feature_index, desc->thresholds,
+                               desc->leaf_values});
     const int32_t n_features = desc->n_features;
     const int device = desc->device;
     const bool u32 = desc->leaf_type == ODF_LEAF_U32;
     if (desc->leaf_type != ODF_LEAF_F32 && !u32)
         return fail(ODF_E_INVALID_ARG, "leaf_type %d unknown", desc->leaf_type);
-    const float *leaf_f = static_cast<const float *>(desc->leaf_values);
-    const uint32_t *leaf_u = static_cast<const uint32_t *>(desc->leaf_values);
-    const void *leaf_values = desc->leaf_values;
     if (u32 && (!std::isfinite(desc->scale) || !std::isfinite(desc->bias)))
         return fail(ODF_E_INVALID_ARG, "scale / bias not finite");
-    if (depth < 0 || depth > ODF_MAX_DEPTH) return fail(ODF_E_INVALID_ARG, "depth %d not in [0, %d]", depth, ODF_MAX_DEPTH);
-    if (n_trees < 0) return fail(ODF_E_INVALID_ARG, "n_trees < 0");
-    if (n_trees > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
     if (n_features < 1) return fail(ODF_E_INVALID_ARG, "n_features < 1");
-    const int64_t n_nodes = n_trees * depth;
-    const int64_t n_leaves = n_trees << depth;
-    if (n_nodes > 0 && (!feature_index || !thresholds))
-        return fail(ODF_E_INVALID_ARG, "feature_index / thresholds is NULL");
-    if (n_leaves > 0 && !leaf_values) return fail(ODF_E_INVALID_ARG, "leaf_values is NULL");
-    for (int64_t k = 0; k < n_nodes; ++k) {
-        if (feature_index[k] < 0 || feature_index[k] >= n_features)
-            return fail(ODF_E_INVALID_ARG, "feature_index[%lld] = %d not in [0, n_features=%d)",
-                        (long long)k, feature_index[k], n_features);
-        if (!std::isfinite(thresholds[k]))
-            return fail(ODF_E_INVALID_ARG, "thresholds[%lld] is not finite", (long long)k);
+    if (segs.size() > static_cast<size_t>(kMaxSegments) || (segs.size() > 1 && !u32))
+        return fail(ODF_E_INVALID_ARG, "mixed-height models: <= %d segments, integer answers", kMaxSegments);
+    int32_t depth = 0;
+    int64_t n_trees = 0, n_leaves = 0;
+    for (const SegSpec &g : segs) {
+        if (g.depth < 0 || g.depth > ODF_MAX_DEPTH)
+            return fail(ODF_E_INVALID_ARG, "depth %d not in [0, %d]", g.depth, ODF_MAX_DEPTH);
+        if (g.n_trees < 0) return fail(ODF_E_INVALID_ARG, "n_trees < 0");
+        if (g.n_trees > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
+        const int64_t nodes = g.n_trees * g.depth, leaves = g.n_trees << g.depth;
+        if (nodes > 0 && (!g.fi || !g.thr)) return fail(ODF_E_INVALID_ARG, "feature_index / thresholds is NULL");
+        if (leaves > 0 && !g.leaves) return fail(ODF_E_INVALID_ARG, "leaf_values is NULL");
+        for (int64_t k = 0; k < nodes; ++k) {
+            if (g.fi[k] < 0 || g.fi[k] >= n_features)
+                return fail(ODF_E_INVALID_ARG, "feature_index[%lld] = %d not in [0, n_features=%d)",
+                            (long long)k, g.fi[k], n_features);
+            if (!std::isfinite(g.thr[k]))
+                return fail(ODF_E_INVALID_ARG, "thresholds[%lld] is not finite", (long long)k);
+        }
+        if (!u32)
+            for (int64_t k = 0; k < leaves; ++k)
+                if (!std::isfinite(static_cast<const float *>(g.leaves)[k]))
+                    return fail(ODF_E_INVALID_ARG, "leaf_values[%lld] is not finite", (long long)k);
+        depth = std::max(depth, g.depth);
+        n_trees += g.n_trees;
+        n_leaves += leaves;
     }
-    if (!u32)
-        for (int64_t k = 0; k < n_leaves; ++k)
-            if (!std::isfinite(leaf_f[k]))
-                return fail(ODF_E_INVALID_ARG, "leaf_values[%lld] is not finite", (long long)k);
-
+    if (n_trees > (int64_t(1) << 30)) return fail(ODF_E_INVALID_ARG, "n_trees > 2^30");
     if (n_leaves > (int64_t(1) << 32))
         return fail(ODF_E_UNSUPPORTED, "%lld answers > 2^32", (long long)n_leaves);
     if (device < 0) return fail(ODF_E_INVALID_ARG, "device %d < 0", device);
+    // uniform-depth models keep the single-depth geometry below (seg 0)
+    const int32_t *feature_index = segs[0].fi;
+    const float *thresholds = segs[0].thr;
+    const float *leaf_f = static_cast<const float *>(segs[0].leaves);
+    const void *leaf_values = segs[0].leaves;
+    const int64_t n_nodes = segs[0].n_trees * segs[0].depth;
 
     std::unique_ptr<odf_model> m(new odf_model());
     m->device = device;
     m->depth = depth;
+    m->kdepth = segs.size() > 1 ? kMixedDepth : depth;
     m->n_trees = n_trees;
     m->n_features = n_features;
     m->leaf_u32 = u32;
@@ -541,7 +610,8 @@ static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out
 
     // ---- borders per factor (sorted, unique by ==) ----
     std::vector<std::vector<float>> borders(n_features);
-    for (int64_t k = 0; k < n_nodes; ++k) borders[feature_index[k]].push_back(thresholds[k]);
+    for (const SegSpec &g : segs)
+        for (int64_t k = 0; k < g.n_trees * g.depth; ++k) borders[g.fi[k]].push_back(g.thr[k]);
     std::vector<int32_t> used_of(n_features, -1), colB_of(n_features, -1);
     for (int32_t f = 0; f < n_features; ++f) {
         auto &b = borders[f];
@@ -653,65 +723,84 @@ static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out
         m->bord_stride = std::max(m->bord_stride, (hi - lo) * 4u);
     }
 
-    // ---- tree chunks: descriptors + reversed leaf tables ----
-    const int dstride = desc_stride(depth);
-    m->table_stride = static_cast<uint32_t>(table_stride(depth));
+    // ---- tree chunks: descriptors + reversed leaf tables, per height segment ----
     // chunk size: about one factor sub-tile (16.5 KB + its borders), so one ring slot
     // carries a sub-tile in phase A or a chunk of similar bytes in phase B and the
     // ring is as deep as shared memory allows (up to 8 stages: more factor data in
     // flight while phase A runs); at least 16 trees (one per consumer warp)
-    {
-        const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
-        const uint32_t per = static_cast<uint32_t>(dstride) + m->table_stride;
-        m->tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, unit / (16u * per)));
-    }
-    m->desc_bytes = align_up(static_cast<uint64_t>(m->tc) * dstride, 256);
-    m->chunk_bytes = m->desc_bytes + static_cast<uint32_t>(m->tc) * m->table_stride;
-    m->n_tchunks = static_cast<int32_t>((n_trees + m->tc - 1) / m->tc);
-    if (static_cast<int64_t>(m->n_tchunks) * m->chunk_bytes > (int64_t(1) << 36))
-        return fail(ODF_E_NOMEM, "tree chunks of %lld bytes > 64 GiB",
-                    (long long)(static_cast<int64_t>(m->n_tchunks) * m->chunk_bytes));
-    std::vector<uint8_t> chunks(static_cast<size_t>(m->n_tchunks) * m->chunk_bytes, 0);
-    // padding trees of the last chunk: -0.0 answers (x + -0.0 == x bit for bit) / 0
-    if (!u32 && n_trees % m->tc != 0) {
-        uint8_t *ch = chunks.data() + static_cast<size_t>(m->n_tchunks - 1) * m->chunk_bytes;
-        for (int64_t i = n_trees % m->tc; i < m->tc; ++i) {
-            float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
-            for (uint32_t F = 0; F < (1u << depth); ++F) tab[F] = -0.0f;
-        }
-    }
-    const uint32_t nleaf = 1u << depth;
-    for (int64_t t = 0; t < n_trees; ++t) {
-        uint8_t *ch = chunks.data() + static_cast<size_t>(t / m->tc) * m->chunk_bytes;
-        const int64_t i = t % m->tc;
-        uint32_t *desc = reinterpret_cast<uint32_t *>(ch + i * dstride);
-        for (int l = 0; l < depth; ++l) {
-            const int32_t f = feature_index[t * depth + l];
-            const float thr = thresholds[t * depth + l];
-            const auto &b = borders[f];
-            const auto it = std::lower_bound(b.begin(), b.end(), thr, [](float a, float c) { return a < c; });
-            const uint32_t k = static_cast<uint32_t>(it - b.begin());  // b[k] == thr
-            // bin <= k  <=>  code of column c = k / 127 <= k - 127c
-            const uint32_t c = k / 127u;
-            const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
-                                        : static_cast<uint32_t>(colB_of[f]) + c - 1u;
-            const uint32_t K = k - 127u * c + 1u;
-            if (desc8(depth)) {
-                desc[2 * l] = col * kTile;
-                desc[2 * l + 1] = (128u - K) * 0x01010101u;
-            } else {
-                desc[l] = (col << 19) | (128u - K);
+    const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
+    std::vector<uint8_t> chunks;
+    int64_t total_chunk_bytes = 0;
+    for (size_t sg = 0; sg < segs.size(); ++sg) {
+        const SegSpec &g = segs[sg];
+        const int sdepth = g.depth;
+        const int dstride = desc_stride(sdepth);
+        const uint32_t tstride = static_cast<uint32_t>(table_stride(sdepth));
+        const uint32_t per = static_cast<uint32_t>(dstride) + tstride;
+        const int32_t tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, unit / (16u * per)));
+        const uint32_t dbytes = align_up(static_cast<uint64_t>(tc) * dstride, 256);
+        const uint32_t cbytes = dbytes + static_cast<uint32_t>(tc) * tstride;
+        const int32_t nch = static_cast<int32_t>((g.n_trees + tc - 1) / tc);
+        total_chunk_bytes += static_cast<int64_t>(nch) * cbytes;
+        if (total_chunk_bytes > (int64_t(1) << 36))
+            return fail(ODF_E_NOMEM, "tree chunks of %lld bytes > 64 GiB", (long long)total_chunk_bytes);
+        const size_t base = chunks.size();
+        chunks.resize(base + static_cast<size_t>(nch) * cbytes, 0);
+        // padding trees of the last chunk: -0.0 answers (x + -0.0 == x bit for bit) / 0
+        if (!u32 && g.n_trees % tc != 0) {
+            uint8_t *ch = chunks.data() + base + static_cast<size_t>(nch - 1) * cbytes;
+            for (int64_t i = g.n_trees % tc; i < tc; ++i) {
+                float *tab = reinterpret_cast<float *>(ch + dbytes + i * tstride);
+                for (uint32_t F = 0; F < (1u << sdepth); ++F) tab[F] = -0.0f;
             }
         }
-        float *tab = reinterpret_cast<float *>(ch + m->desc_bytes + i * m->table_stride);
-        if (u32) {
-            uint32_t *tab_u = reinterpret_cast<uint32_t *>(tab);
-            for (uint32_t F = 0; F < nleaf; ++F)
-                tab_u[leaf_pos(depth, F)] = leaf_u[t * nleaf + (nleaf - 1 - F)];
-        } else {
-            for (uint32_t F = 0; F < nleaf; ++F)
-                tab[leaf_pos(depth, F)] = leaf_f[t * nleaf + (nleaf - 1 - F)];
+        const uint32_t nleaf = 1u << sdepth;
+        const float *lf = static_cast<const float *>(g.leaves);
+        const uint32_t *lu = static_cast<const uint32_t *>(g.leaves);
+        for (int64_t t = 0; t < g.n_trees; ++t) {
+            uint8_t *ch = chunks.data() + base + static_cast<size_t>(t / tc) * cbytes;
+            const int64_t i = t % tc;
+            uint32_t *desc = reinterpret_cast<uint32_t *>(ch + i * dstride);
+            for (int l = 0; l < sdepth; ++l) {
+                const int32_t f = g.fi[t * sdepth + l];
+                const float thr = g.thr[t * sdepth + l];
+                const auto &b = borders[f];
+                const auto it = std::lower_bound(b.begin(), b.end(), thr, [](float a, float c) { return a < c; });
+                const uint32_t k = static_cast<uint32_t>(it - b.begin());  // b[k] == thr
+                // bin <= k  <=>  code of column c = k / 127 <= k - 127c
+                const uint32_t c = k / 127u;
+                const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
+                                            : static_cast<uint32_t>(colB_of[f]) + c - 1u;
+                const uint32_t K = k - 127u * c + 1u;
+                if (desc8(sdepth)) {
+                    desc[2 * l] = col * kTile;
+                    desc[2 * l + 1] = (128u - K) * 0x01010101u;
+                } else {
+                    desc[l] = (col << 19) | (128u - K);
+                }
+            }
+            uint8_t *tab = ch + dbytes + i * tstride;
+            for (uint32_t F = 0; F < nleaf; ++F) {
+                const size_t src = static_cast<size_t>(t) * nleaf + (nleaf - 1 - F);
+                if (u32)
+                    reinterpret_cast<uint32_t *>(tab)[leaf_pos(sdepth, F)] = lu[src];
+                else
+                    reinterpret_cast<float *>(tab)[leaf_pos(sdepth, F)] = lf[src];
+            }
         }
+        if (sg == 0) {  // the uniform geometry (a mixed model's slot is sized below)
+            m->tc = tc;
+            m->desc_bytes = dbytes;
+            m->chunk_bytes = cbytes;
+            m->table_stride = tstride;
+        }
+        if (segs.size() > 1)
+            m->seg[sg] = SegP{sdepth, tc, nch, cbytes, dbytes, 0u, static_cast<uint64_t>(base)};
+        m->n_tchunks += nch;
+    }
+    if (segs.size() > 1) {
+        m->n_seg = static_cast<int32_t>(segs.size());
+        for (int sg = 0; sg < m->n_seg; ++sg) m->chunk_bytes = std::max(m->chunk_bytes, m->seg[sg].chunk_bytes);
     }
 
     // ---- NEXT-3: binary features (used factor u, border j) and per-level word offsets ----
@@ -719,7 +808,7 @@ static odf_status load_model_ex_impl(const odf_model_desc *desc, odf_model **out
     for (int32_t u = 0; u < m->n_used; ++u)
         bf_base[u + 1] = bf_base[u] + static_cast<uint32_t>(borders[m->used_ids[u]].size());
     std::vector<uint32_t> bits_desc;
-    if (!u32) {
+    if (!u32 && segs.size() == 1) {
         bits_desc.resize(static_cast<size_t>(n_nodes));
         for (int64_t k = 0; k < n_nodes; ++k) {
             const int32_t f = feature_index[k];
@@ -861,7 +950,8 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != m->device) cudaSetDevice(m->device);
-    cudaError_t e = launch_main(mode, m->depth, p, tmp, grid_for(m, pl, p.n_tiles), pl.smem, s, halves);
+    cudaError_t e = launch_main(mode, mode == MODE_BINARIZE ? 0 : m->kdepth, p, tmp,
+                                grid_for(m, pl, p.n_tiles), pl.smem, s, halves);
     if (prev != m->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     return ok();
@@ -1041,6 +1131,9 @@ static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n
                             int64_t doc0, int64_t ndoc, int64_t tree0, int64_t ntree,
                             uint16_t *d_idx, uint64_t *d_fp, cudaStream_t s)
 {
+    if (m->n_seg > 0)
+        return fail(ODF_E_UNSUPPORTED, "leaf-index export: uniform-depth models only (this one has %d "
+                                       "height segments)", m->n_seg);
     KParams p = base_params(m, m->apply);
     p.n_docs = n_docs;
     p.n_tiles = (n_docs + kTile - 1) / kTile;

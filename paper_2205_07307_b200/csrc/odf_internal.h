@@ -46,6 +46,18 @@ __host__ __device__ constexpr int trees_per_chunk(int depth)
 
 enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 
+// Mixed-height models (NEXT-2, the paper's native layout): the forest is a
+// list of height segments, each with its own tree-chunk geometry, concatenated in
+// one chunk stream; kernels instantiated with DEPTH = kMixedDepth apply each chunk
+// with its segment's depth (integer answers: the u64 sum is order-free).
+constexpr int kMixedDepth = 11;
+constexpr int kMaxSegments = 11;  // heights 0..10
+struct SegP {
+    int32_t depth, tc, n_chunks;
+    uint32_t chunk_bytes, desc_bytes, pad_;
+    uint64_t byte_off;  // of the segment's first chunk in `chunks`
+};
+
 // Per-launch parameters (passed by value; all pointers are device pointers).
 struct KParams {
     // ---- binarization (stage 1) ----
@@ -72,6 +84,9 @@ struct KParams {
     const uint2 *ucols;     // wide models: [n_used] {first extra code column * 128 or trash, C}
     uint32_t off_stage;     // wide models: shared-memory staging of a u16 bins tile
     int32_t n_used, n_cols;
+    // ---- mixed-height models (DEPTH = kMixedDepth) ----
+    int32_t n_seg;
+    SegP seg[kMaxSegments];
     // ---- problem ----
     int64_t n_docs, n_tiles;
     const uint8_t *bins_in;  // blocked bins (apply / index kernels)
@@ -113,6 +128,7 @@ const void *kptr_fused_nu(int depth);  // fused, u32 leaves (NEXT-1)
 const void *kptr_fused_wf(int depth);  // fused, wide models (NEXT-4), fp32 leaves
 const void *kptr_fused_wu(int depth);  // fused, wide models, u32 leaves
 const void *kptr_apply(int depth, bool u32);
+const void *kptr_mixed(int mode);      // mixed-height integer models, fused / apply
 const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
 const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);

@@ -36,6 +36,8 @@ cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cu
 // ---------------------------------------------------------------------------
 static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide = false, int halves = 1)
 {
+    if (depth == kMixedDepth)
+        return (u32 && !wide && halves == 1 && mode != MODE_BINARIZE) ? kptr_mixed(mode) : nullptr;
     if (depth < 0 || depth > 10) return nullptr;
     if (halves == 2) {  // 256-document tiles: fp32 narrow fused / apply only
         if (u32 || wide) return nullptr;
@@ -131,6 +133,10 @@ cudaError_t prepare_kernels(int max_smem)
             cudaError_t e = opt_in(f, max_smem);
             if (e != cudaSuccess) return e;
         }
+    }
+    for (int mode : {MODE_FUSED, MODE_APPLY}) {
+        cudaError_t e = opt_in(main_kernel(mode, kMixedDepth, true), max_smem);
+        if (e != cudaSuccess) return e;
     }
     cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
     if (e != cudaSuccess) return e;

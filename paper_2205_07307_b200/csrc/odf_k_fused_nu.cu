@@ -10,6 +10,14 @@ static const void *fn()
     return reinterpret_cast<const void *>(&odf_main_kernel<MODE_FUSED, DEPTH, true, false>);
 }
 
+// mixed-height integer models (NEXT-2): depth argument kMixedDepth
+const void *kptr_mixed(int mode)
+{
+    return mode == MODE_FUSED
+               ? reinterpret_cast<const void *>(&odf_main_kernel<MODE_FUSED, kMixedDepth, true, false>)
+               : reinterpret_cast<const void *>(&odf_main_kernel<MODE_APPLY, kMixedDepth, true, false>);
+}
+
 const void *kptr_fused_nu(int depth)
 {
     static const void *t[11] = {fn<0>(), fn<1>(), fn<2>(), fn<3>(), fn<4>(), fn<5>(),

@@ -894,6 +894,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr bool HAS_B = MODE != MODE_BINARIZE;
     constexpr int kTileH = kTile * H;            // documents per tile
     constexpr int kSlots = kConsumerWarps / H;   // tree slots per half (phase B)
+    constexpr bool MIXED = DEPTH == kMixedDepth;  // per-segment depths (NEXT-2)
+    static_assert(!MIXED || (H == 1 && U32), "mixed-height models: integer answers, 128-doc tiles");
     static_assert(H == 1 || (H == 2 && !WIDE && MODE != MODE_BINARIZE), "halves: fused/apply, narrow");
     if (smem_addr(smem_raw) & 1023u) __trap();  // alignment the TMA swizzle relies on
     const uint32_t base = 0;
@@ -910,7 +912,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_fjobs = HAS_A ? (p.n_fchunks + p.fsub_per_job - 1) / p.fsub_per_job : 0;
     // ring jobs of phase B: tree chunks (H = 1) or half-chunks of tc / 2 trees (H = 2)
-    const int n_bjobs = HAS_B ? p.n_tchunks * H : 0;
+    const int n_bjobs = HAS_B && !MIXED ? p.n_tchunks * H : 0;
     constexpr bool WIDE_BINS = MODE == MODE_BINARIZE && WIDE;
     const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile * (p.wide ? 2u : 1u);
     const uint32_t bins_dst = (MODE == MODE_APPLY && p.wide) ? base + p.off_stage : bins;
@@ -973,6 +975,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, full);
                     }
                     if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+                }
+                if constexpr (MIXED) {  // every segment's chunks, in segment order
+                    for (int sg = 0; sg < p.n_seg; ++sg)
+                        for (int c = 0; c < p.seg[sg].n_chunks; ++c) {
+                            const uint32_t full = bars + 16u * slot, empty = full + 8u;
+                            mbar_wait(empty, ph ^ 1u);
+                            const uint32_t cb = p.seg[sg].chunk_bytes;
+                            mbar_expect_tx(full, cb);
+                            bulk_g2s(ring + slot * p.slot_bytes,
+                                     p.chunks + p.seg[sg].byte_off + static_cast<size_t>(c) * cb, cb, full);
+                            if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+                        }
                 }
                 for (int c = 0; c < n_bjobs; ++c) {
                     const uint32_t full = bars + 16u * slot, empty = full + 8u;
@@ -1055,6 +1069,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         // acc: the group of the warp's next tree; acc2 (H = 2): the other group
         Acc<U32> acc, acc2;
+        if constexpr (MIXED) {
+            for (int sg = 0; sg < p.n_seg; ++sg) {
+                const int sd = p.seg[sg].depth, snk = p.seg[sg].tc / kConsumerWarps;
+                const uint32_t sdesc = p.seg[sg].desc_bytes;
+                for (int c = 0; c < p.seg[sg].n_chunks; ++c) {
+                    const uint32_t full = bars + 16u * slot, empty = full + 8u;
+                    mbar_wait(full, ph);
+                    const uint32_t sb = ring + slot * p.slot_bytes;
+                    switch (sd) {  // warp-uniform: one branch per chunk
+                        case 0: apply_chunk<0, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 1: apply_chunk<1, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 2: apply_chunk<2, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 3: apply_chunk<3, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 4: apply_chunk<4, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 5: apply_chunk<5, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 6: apply_chunk<6, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 7: apply_chunk<7, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 8: apply_chunk<8, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 9: apply_chunk<9, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        default: apply_chunk<10, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                    }
+                    acc.pin(pin_scratch);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty);
+                    if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
+                }
+            }
+        }
         for (int c = 0; c < n_bjobs; ++c) {
             const uint32_t full = bars + 16u * slot, empty = full + 8u;
             DIAG_T(tw0);
@@ -1067,7 +1109,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n_bjobs < 0)
 #endif
             {
-                if constexpr (H == 1) {
+                if constexpr (MIXED) {
+                } else if constexpr (H == 1) {
                     apply_chunk<DEPTH, U32>(sb, desc_off, ln, tslot, nk, acc);
                 } else {
 #pragma unroll 2

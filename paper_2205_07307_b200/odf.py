@@ -59,7 +59,7 @@ class _PaperDesc(ctypes.Structure):
                 ("thresholds", ctypes.c_void_p), ("stc", ctypes.c_void_p),
                 ("cond_indices", ctypes.c_void_p), ("leaves", ctypes.c_void_p),
                 ("scale", ctypes.c_double), ("bias", ctypes.c_double),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("pad_heights", ctypes.c_int32)]
 
 
 _lib = None
@@ -211,8 +211,9 @@ class Model:
 
     @classmethod
     def from_paper(cls, n_features, group_factor, group_count, thresholds, stc, cond_indices,
-                   leaves, scale=1.0, bias=0.0, device: int = 0) -> "Model":
-        """Import the paper's model layout: see odf_load_model_paper."""
+                   leaves, scale=1.0, bias=0.0, device: int = 0, pad_heights: bool = False) -> "Model":
+        """Import the paper's model layout: see odf_load_model_paper
+        (per-height segments; pad_heights=True: the padded uniform-depth form)."""
         gf = np.ascontiguousarray(group_factor, dtype=np.int32)
         gc = np.ascontiguousarray(group_count, dtype=np.int32)
         th = np.ascontiguousarray(thresholds, dtype=np.float32)
@@ -224,7 +225,7 @@ class Model:
                        gc.ctypes.data if gc.size else None, gf.size,
                        th.ctypes.data if th.size else None, st.ctypes.data,
                        ci.ctypes.data if ci.size else None, lv.ctypes.data if lv.size else None,
-                       float(scale), float(bias), int(device))
+                       float(scale), float(bias), int(device), 1 if pad_heights else 0)
         h = _vp()
         _check(lib().odf_load_model_paper(ctypes.byref(d), ctypes.byref(h)))
         self = cls.__new__(cls)

@@ -526,13 +526,15 @@ def test_integer_leaves_exact(depth, n_docs, n_trees):
 # ---------------------------------------------------------------------------
 # NEXT-2: paper-native mixed-height model import, exact u64 parity
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("pad_heights", [False, True], ids=["per_height", "padded"])
 @pytest.mark.parametrize("stc,n_binary,n_features", [
     ([100] * 9, 100, 100),             # Table 6.1 synthetic: 100 trees of each height 0..8
     ([3, 0, 5, 0, 0, 0, 40, 0, 0], 150, 20),
     ([0, 0, 0, 0, 0, 0, 64, 0, 0], 64, 64),
     ([7, 0, 0, 0, 0, 0, 0, 0, 0], 10, 4),   # only constant (height-0) trees
+    ([1, 1, 1, 1, 1, 1, 1990, 2, 3], 2000, 500),  # P:168's mix: ~99.9 % depth 6
 ])
-def test_paper_native_import(stc, n_binary, n_features):
+def test_paper_native_import(stc, n_binary, n_features, pad_heights):
     import torch
     from paper_2205_07307_b200 import Model
     pm = synth.paper_model(11, n_features, n_binary, stc)
@@ -546,12 +548,22 @@ def test_paper_native_import(stc, n_binary, n_features):
         f = np.repeat(pm.group_factor, pm.group_count)[k]
         x[rng.integers(D), f] = pm.thresholds[k]
     m = Model.from_paper(pm.n_features, pm.group_factor, pm.group_count, pm.thresholds, pm.stc,
-                         pm.cond_indices, pm.leaves, pm.scale, pm.bias)
-    sums, sc = m.score_u64(torch.from_numpy(x).cuda())
+                         pm.cond_indices, pm.leaves, pm.scale, pm.bias, pad_heights=pad_heights)
+    xd = torch.from_numpy(x).cuda()
+    sums, sc = m.score_u64(xd)
     want = oracle.apply_paper(x, pm.group_factor, pm.group_count, pm.thresholds, pm.stc,
                               pm.cond_indices, pm.leaves)
     assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
     assert np.array_equal(sc.cpu().numpy(), oracle.finalize(want, pm.scale, pm.bias))
+    # two-stage (binarize + apply_u64) gives the same exact sums
+    s2, _ = m.apply_u64(m.binarize(xd), D)
+    assert np.array_equal(s2.cpu().numpy().view(np.uint64), want)
+    heights = [h for h in range(len(stc)) if stc[h] > 0]
+    if not pad_heights and len(heights) > 1:  # mixed model: no per-tree index export
+        from paper_2205_07307_b200 import OdfError
+        with pytest.raises(OdfError) as e:
+            m.index_fingerprint(m.binarize(xd), D)
+        assert e.value.status == 2
     m.close()
 
 

@@ -105,3 +105,52 @@ def test_two_rank_doc_and_tree_sharding(exact):
         if exact:
             assert np.array_equal(tree, s32)  # exact partial sums: bit-exact
     assert np.abs(res[0][2] - s64).max() <= tol  # reduce to root
+
+
+def _worker_bench_shard(rank, world, port, n_docs, q):
+    """bench.py --gpus N (doc sharding) host logic: rank r generates only its rows of
+    the batch (synth rows=), scores them, and the padded all-gather into a
+    preallocated buffer rebuilds the whole score vector on every rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    import oracle
+    import synth
+    from paper_2205_07307_b200.parallel import DocSharded
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard_bounds(n_docs, world, rank)
+        case = synth.make_case("c2", n_docs=n_docs, n_trees=40, rows=(lo, hi))
+        assert case.x.shape[0] == hi - lo
+        _, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values,
+                              case.depth)
+        ds = DocSharded(lambda t: t)
+        m = DocSharded.padded_size(n_docs, world)
+        loc = torch.zeros(m, dtype=torch.float32)
+        loc[:hi - lo] = torch.from_numpy(s32)
+        out = torch.empty(m * world, dtype=torch.float32)
+        ds.gather_into(loc, out)
+        q.put((rank, ds.unpad(out, n_docs).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_docs", [(2, 3001), (3, 1000)])
+def test_bench_doc_shard_gather(world, n_docs):
+    import oracle
+    import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_bench_shard, args=(r, world, port, n_docs, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    case = synth.make_case("c2", n_docs=n_docs, n_trees=40)
+    _, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, case.depth)
+    for r in range(world):
+        assert np.array_equal(res[r].view(np.uint32), s32.view(np.uint32))

@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 KEYS = {
-    "duration_ns": "gpu__time_duration.sum",
+    "duration_ms": "gpu__time_duration.sum",
     "dram_read": "dram__bytes_read.sum",
     "dram_write": "dram__bytes_write.sum",
     "lts_bytes": "lts__t_bytes.sum",
@@ -54,11 +54,13 @@ def main():
             if m in d:
                 v = _num(d[m])
                 u = units[hdr.index(m)]
-                if v is not None and u in ("Kbyte", "Mbyte", "Gbyte", "usecond", "msecond", "Mhz",
-                                            "Ghz", "cycle/usecond", "cycle/nsecond"):
-                    v *= {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e3,
-                          "msecond": 1e6, "Mhz": 1e6, "Ghz": 1e9, "cycle/usecond": 1e6,
-                          "cycle/nsecond": 1e9}[u]
+                # normalise: bytes, milliseconds, Hz
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                         "ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1,
+                         "msecond": 1, "s": 1e3, "second": 1e3, "hz": 1, "Khz": 1e3, "Mhz": 1e6,
+                         "Ghz": 1e9, "cycle/usecond": 1e6, "cycle/nsecond": 1e9}
+                if v is not None and u in scale:
+                    v *= scale[u]
                 e[k] = v
         res.append(e)
     print(json.dumps(res if "--all" in sys.argv else res[0], indent=1))
