@@ -304,7 +304,18 @@ def run_ours(args):
 
     ws, rank, local = _dist()
     if ws > 1:
+        # NCCL's communicator-init lines (nranks, transports) on stderr, so the one
+        # JSON line stays alone on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        probe = torch.ones(1, device=torch.device("cuda", local))
+        dist.all_reduce(probe)  # creates the communicator now
+        if rank == 0:
+            print(f"[bench] NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}: communicator "
+                  f"nranks={dist.get_world_size()} (all-reduce probe = {int(probe.item())})",
+                  file=sys.stderr, flush=True)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import synth
