@@ -161,12 +161,17 @@ typedef struct {
     int32_t max_tile_docs;      /* 256 if 256-document tiles fit (odf_score_tiles), else 128 */
     int32_t stages_fused_256;   /* ring stages of the fused kernel with 256-document tiles (0: none) */
     int32_t smem_fused_256;     /* its dynamic shared memory per CTA, bytes (0: none) */
+    int32_t bins_tile_docs;     /* documents per tile and per bins block: ODF_TILE_DOCS (128), or 64
+                                   for models whose 128-document code block does not fit shared
+                                   memory (about > 1,600 code columns, e.g. P:168's 1,950 factors;
+                                   at depth 9-10 such widths do not fit at all: ODF_E_UNSUPPORTED) */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);
 
 /* Bytes of the blocked bins buffer for n_docs documents
- * (= ceil(n_docs/ODF_TILE_DOCS) * n_used * ODF_TILE_DOCS * bins_elem_bytes), the number of used
+ * (= ceil(n_docs/TD) * n_used * TD * bins_elem_bytes, TD = odf_model_info.bins_tile_docs:
+ * layout [ceil(n_docs/TD)][n_used][TD], document d of a block at byte d), the number of used
  * features, and (optional, may be NULL) a library-owned pointer to their raw
  * ids, ascending, valid until odf_free_model.                                */
 ODF_API odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,

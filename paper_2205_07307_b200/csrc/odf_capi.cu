@@ -99,6 +99,7 @@ struct odf_model {
     int device = 0, num_sms = 0, max_smem = 0;
     int32_t depth = 0, n_features = 0;
     int32_t kdepth = 0;  // kernel instantiation: depth, or kMixedDepth for mixed-height models
+    int32_t tile_docs = kTile;  // 128, or 64 when a 128-document code block does not fit (DPL = 2)
     int32_t n_seg = 0;   // mixed-height models (NEXT-2): height segments of the chunk stream
     SegP seg[kMaxSegments] = {};
     int64_t n_trees = 0;
@@ -145,15 +146,17 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
     // of a wide model stages the u16 bins tile next to the code columns it expands
     // them into
     const uint32_t elem = (mode == MODE_BINARIZE && m.wide) ? 2u : 1u;
-    const uint32_t half_bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile * elem, 1024);
+    const uint32_t td = static_cast<uint32_t>(m.tile_docs);  // documents per tile (half)
+    const uint32_t half_bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * td * elem, 1024);
     const uint32_t bins = half_bins * static_cast<uint32_t>(halves);
     const uint32_t stage = (mode == MODE_APPLY && m.wide)
                                ? align_up(static_cast<uint64_t>(m.n_used) * kTile * 2, 1024) : 0u;
-    const uint32_t red_bytes = (m.leaf_u32 ? 2 * kRedBytes : kRedBytes) * static_cast<uint32_t>(halves);
+    const uint32_t red_bytes = (m.leaf_u32 ? 2 * kRedBytes : kRedBytes) * static_cast<uint32_t>(halves) * td / kTile;
     const uint32_t bins_region = ((mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes)) + stage;
     const uint32_t bars = align_up(160 + 8u * m.n_fchunks, 128);  // barriers, scratch, bchunk copy
     // a factor sub-tile travels as [halves x 16 KB boxes][512 B fmeta][its border arrays]
-    const uint32_t unit = kFSubBytes * halves + kMetaBytes + m.bord_stride;
+    const uint32_t box = td * kFSub * 4u;  // one TMA box: td documents x 32 factors
+    const uint32_t unit = box * halves + kMetaBytes + m.bord_stride;
     // tree jobs: whole chunks, or (halves == 2) half-chunks of tc / 2 trees
     uint32_t hdesc = 0, tree_slot;
     if (halves == 1) {
@@ -180,8 +183,8 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
     if (pl.stages < 2) {
         char b[256];
         snprintf(b, sizeof b,
-                 "shared memory: %d x %d code columns x 128 B + 2 x %u B slots do not fit %d B", halves,
-                 m.n_cols, slot, m.max_smem);
+                 "shared memory: %d x %d code columns x %u documents + 2 x %u B ring slots do not fit %d B",
+                 halves, m.n_cols + 1, td, slot, m.max_smem);
         why = b;
         return false;
     }
@@ -190,7 +193,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
     pl.hdesc_bytes = hdesc;
     pl.slot_bytes = slot;
     pl.fsub = std::max<int>(1, static_cast<int>(slot / unit));
-    pl.off_meta = pl.fsub * halves * kFSubBytes;
+    pl.off_meta = pl.fsub * halves * box;
     pl.off_bord = pl.off_meta + pl.fsub * kMetaBytes;
     uint32_t off = 0;
     pl.off_ring = off;                    // ring first: TMA swizzle needs 1024 B alignment
@@ -223,8 +226,8 @@ odf_status encode_tmap(const odf_model *m, const float *d_x, int64_t n_docs, int
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(fm ? n_docs : m->n_features),
                           static_cast<cuuint64_t>(fm ? m->n_features : n_docs)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(fm ? kTile : kFSub),
-                         static_cast<cuuint32_t>(fm ? kFSub : kTile)};
+    const cuuint32_t td = static_cast<cuuint32_t>(m->tile_docs);  // documents per tile
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(fm ? td : kFSub), static_cast<cuuint32_t>(fm ? kFSub : td)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(d_x), dims,
                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -257,6 +260,7 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.n_used = m->n_used;
     p.n_cols = m->n_cols;
     p.code_stride = static_cast<int64_t>(m->n_cols + 1) * kTile;
+    p.tile_docs = m->tile_docs;
     p.off_bins = pl.off_bins;
     p.off_ring = pl.off_ring;
     p.off_red = pl.off_red;
@@ -862,14 +866,23 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         return cuda_fail(e, "cudaFuncSetAttribute");
     }
     std::string why;
-    if (!make_plan(*m, MODE_FUSED, m->fused, why) || !make_plan(*m, MODE_APPLY, m->apply, why) ||
-        !make_plan(*m, MODE_BINARIZE, m->binz, why)) {
+    auto plans = [&]() {
+        return make_plan(*m, MODE_FUSED, m->fused, why) && make_plan(*m, MODE_APPLY, m->apply, why) &&
+               make_plan(*m, MODE_BINARIZE, m->binz, why);
+    };
+    bool planned = plans();
+    if (!planned && !m->wide) {  // a 128-document code block does not fit: 64-document tiles
+        m->tile_docs = kTile / 2;
+        why.clear();
+        planned = plans();
+    }
+    if (!planned) {
         odf_free_model(m.release());
         return fail(ODF_E_UNSUPPORTED, "%s", why.c_str());
     }
-    m->binz.grid_per_sm = occupancy_main(MODE_BINARIZE, 0, m->binz.smem);
+    m->binz.grid_per_sm = occupancy_main(MODE_BINARIZE, 0, m->binz.smem, m->tile_docs);
     // 256-document tiles (two halves), fp32 narrow models, when two code blocks fit
-    if (!m->leaf_u32 && !m->wide) {
+    if (!m->leaf_u32 && !m->wide && m->tile_docs == kTile) {
         std::string why2;
         if (!make_plan(*m, MODE_FUSED, m->fused2, why2, 2)) m->fused2 = Plan();
         if (!make_plan(*m, MODE_APPLY, m->apply2, why2, 2)) m->apply2 = Plan();
@@ -906,7 +919,8 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->leaf_type = m->leaf_u32 ? ODF_LEAF_U32 : ODF_LEAF_F32;
     info->bord_stride = static_cast<int32_t>(m->bord_stride);
     info->bins_elem_bytes = m->wide ? 2 : 1;
-    info->max_tile_docs = m->fused2.valid ? 2 * kTile : kTile;
+    info->max_tile_docs = m->fused2.valid ? 2 * kTile : m->tile_docs;
+    info->bins_tile_docs = m->tile_docs;
     info->stages_fused_256 = m->fused2.valid ? m->fused2.stages : 0;
     info->smem_fused_256 = m->fused2.valid ? static_cast<int32_t>(m->fused2.smem) : 0;
     return ok();
@@ -917,8 +931,9 @@ odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
 {
     if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
     if (n_docs < 0) return fail(ODF_E_INVALID_ARG, "n_docs < 0");
-    const int64_t tiles = (n_docs + kTile - 1) / kTile;
-    if (bytes) *bytes = static_cast<size_t>(tiles) * m->n_used * kTile * (m->wide ? 2 : 1);
+    const int64_t td = m->tile_docs;
+    const int64_t tiles = (n_docs + td - 1) / td;
+    if (bytes) *bytes = static_cast<size_t>(tiles) * m->n_used * td * (m->wide ? 2 : 1);
     if (n_used_features) *n_used_features = m->n_used;
     if (used_feature_ids) *used_feature_ids = m->used_ids.empty() ? nullptr : m->used_ids.data();
     return ok();
@@ -933,7 +948,7 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
                                  : mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
     KParams p = base_params(m, pl);
     p.n_docs = n_docs;
-    p.n_tiles = (n_docs + kTile * halves - 1) / (kTile * halves);
+    p.n_tiles = (n_docs + m->tile_docs * halves - 1) / (m->tile_docs * halves);
     p.bins_in = bins_in;
     p.bins_out = bins_out;
     p.scores = scores;
@@ -1057,7 +1072,7 @@ odf_status odf_bits_from_bins(const odf_model *m, const uint8_t *d_bins, int64_t
     if (!d_bins || !d_words) return fail(ODF_E_INVALID_ARG, "NULL buffer");
     KParams p = base_params(m, m->apply);
     p.n_docs = n_docs;
-    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.n_tiles = (n_docs + m->tile_docs - 1) / m->tile_docs;
     p.bins_in = d_bins;
     p.bf_base = m->d_bf_base;
     p.k_bin = m->total_borders;
@@ -1136,7 +1151,8 @@ static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n
                                        "height segments)", m->n_seg);
     KParams p = base_params(m, m->apply);
     p.n_docs = n_docs;
-    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    const int64_t td = m->tile_docs;
+    p.n_tiles = (n_docs + td - 1) / td;
     p.bins_in = d_bins;
     p.doc0 = doc0;
     p.ndoc = ndoc;
@@ -1145,9 +1161,9 @@ static odf_status run_index(const odf_model *m, const uint8_t *d_bins, int64_t n
     p.idx_out = d_idx;
     p.fp_out = d_fp;
     const int grid = fp ? static_cast<int>(p.n_tiles)
-                        : static_cast<int>((doc0 + ndoc - 1) / kTile - doc0 / kTile + 1);
+                        : static_cast<int>((doc0 + ndoc - 1) / td - doc0 / td + 1);
     const int dstride = desc_stride(m->depth);
-    size_t smem = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
+    size_t smem = align_up(static_cast<uint64_t>(m->n_cols) * td, 1024) +
                   align_up(static_cast<uint64_t>(m->tc) * dstride, 1024);
     if (m->wide) {  // u16 bins staged after the descriptors
         p.off_stage = static_cast<uint32_t>(smem);
@@ -1229,6 +1245,9 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    if (m->tile_docs != kTile)
+        return fail(ODF_E_UNSUPPORTED, "latency path: 128-document tiles only (this model uses %d)",
+                    m->tile_docs);
     if ((n_docs + kTile - 1) / kTile > 65535)  // tiles are the grid's y dimension
         return fail(ODF_E_INVALID_ARG, "latency path: n_docs > 65535 x 128 (use odf_score)");
     const int sp = lat_splits(m, n_docs, splits);

@@ -88,6 +88,7 @@ struct KParams {
     int32_t n_seg;
     SegP seg[kMaxSegments];
     // ---- problem ----
+    int32_t tile_docs;       // the model's tile width: 128, or 64 (wide-column models, DPL = 2)
     int64_t n_docs, n_tiles;
     const uint8_t *bins_in;  // blocked bins (apply / index kernels)
     uint8_t *bins_out;       // blocked bins (binarize)
@@ -129,12 +130,17 @@ const void *kptr_fused_wf(int depth);  // fused, wide models (NEXT-4), fp32 leav
 const void *kptr_fused_wu(int depth);  // fused, wide models, u32 leaves
 const void *kptr_apply(int depth, bool u32);
 const void *kptr_mixed(int mode);      // mixed-height integer models, fused / apply
+// 64-document tiles (DPL = 2): fp32 fused / apply (depth) and binarize; u32 fused / apply
+// (depth 0..10 or kMixedDepth); index export
+const void *kptr_t64_f(int mode, int depth);
+const void *kptr_t64_u(int mode, int depth);
+const void *kptr_t64_index(int depth);
 const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
 const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);
 
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
-                        size_t smem, cudaStream_t s, int halves = 1);
+                        size_t smem, cudaStream_t s, int halves = 1);  // p.tile_docs picks DPL
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
                          cudaStream_t s);
 cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,
@@ -143,6 +149,6 @@ cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cu
 // Opt every kernel in to `smem` bytes of dynamic shared memory.
 cudaError_t prepare_kernels(int max_smem);
 // Number of co-resident CTAs per SM of a main kernel at `smem` bytes.
-int occupancy_main(int mode, int depth, size_t smem);
+int occupancy_main(int mode, int depth, size_t smem, int tile_docs = 128);
 
 }  // namespace odf

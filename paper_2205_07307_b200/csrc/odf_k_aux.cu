@@ -34,8 +34,13 @@ cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cu
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide = false, int halves = 1)
+static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide = false, int halves = 1,
+                               int tile_docs = 128)
 {
+    if (tile_docs == 64) {  // 64-document tiles: narrow models, one half
+        if (wide || halves != 1) return nullptr;
+        return u32 ? kptr_t64_u(mode, depth) : kptr_t64_f(mode, depth);
+    }
     if (depth == kMixedDepth)
         return (u32 && !wide && halves == 1 && mode != MODE_BINARIZE) ? kptr_mixed(mode) : nullptr;
     if (depth < 0 || depth > 10) return nullptr;
@@ -55,8 +60,9 @@ static const void *index_fn()
 {
     return reinterpret_cast<const void *>(&odf_index_kernel<DEPTH>);
 }
-static const void *index_kernel(int depth)
+static const void *index_kernel(int depth, int tile_docs = 128)
 {
+    if (tile_docs == 64) return kptr_t64_index(depth);
     static const void *t[11] = {index_fn<0>(), index_fn<1>(), index_fn<2>(), index_fn<3>(),
                                 index_fn<4>(), index_fn<5>(), index_fn<6>(), index_fn<7>(),
                                 index_fn<8>(), index_fn<9>(), index_fn<10>()};
@@ -128,14 +134,21 @@ cudaError_t prepare_kernels(int max_smem)
                             main_kernel(MODE_FUSED, d, true), main_kernel(MODE_APPLY, d, true),
                             main_kernel(MODE_FUSED, d, false, true), main_kernel(MODE_FUSED, d, true, true),
                             main_kernel(MODE_FUSED, d, false, false, 2), main_kernel(MODE_APPLY, d, false, false, 2),
-                            index_kernel(d), lat_apply_kernel(d)};
+                            main_kernel(MODE_FUSED, d, false, false, 1, 64), main_kernel(MODE_APPLY, d, false, false, 1, 64),
+                            main_kernel(MODE_FUSED, d, true, false, 1, 64), main_kernel(MODE_APPLY, d, true, false, 1, 64),
+                            index_kernel(d), index_kernel(d, 64), lat_apply_kernel(d)};
         for (const void *f : fs) {
             cudaError_t e = opt_in(f, max_smem);
             if (e != cudaSuccess) return e;
         }
     }
-    for (int mode : {MODE_FUSED, MODE_APPLY}) {
-        cudaError_t e = opt_in(main_kernel(mode, kMixedDepth, true), max_smem);
+    for (int mode : {MODE_FUSED, MODE_APPLY})
+        for (int td : {128, 64}) {
+            cudaError_t e = opt_in(main_kernel(mode, kMixedDepth, true, false, 1, td), max_smem);
+            if (e != cudaSuccess) return e;
+        }
+    {
+        cudaError_t e = opt_in(main_kernel(MODE_BINARIZE, 0, false, false, 1, 64), max_smem);
         if (e != cudaSuccess) return e;
     }
     cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
@@ -145,11 +158,11 @@ cudaError_t prepare_kernels(int max_smem)
     return opt_in(main_kernel(MODE_BINARIZE, 0), max_smem);
 }
 
-int occupancy_main(int mode, int depth, size_t smem)
+int occupancy_main(int mode, int depth, size_t smem, int tile_docs)
 {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, main_kernel(mode, depth), kThreads,
-                                                      smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, main_kernel(mode, depth, false, false, 1, tile_docs),
+                                                      kThreads, smem) != cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
 }
@@ -157,7 +170,7 @@ int occupancy_main(int mode, int depth, size_t smem)
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s, int halves)
 {
-    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0, halves);
+    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0, halves, p.tile_docs);
     if (!f) return cudaErrorInvalidValue;
     KParams pc = p;
     CUtensorMap tm;
@@ -172,7 +185,7 @@ cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
                          cudaStream_t s)
 {
-    const void *f = index_kernel(depth);
+    const void *f = index_kernel(depth, p.tile_docs);
     if (!f) return cudaErrorInvalidValue;
     KParams pc = p;
     int fp = fingerprint ? 1 : 0;

@@ -100,6 +100,12 @@ __device__ __forceinline__ uint32_t ldsa_u32(uint32_t a)
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
     return r;
 }
+__device__ __forceinline__ uint32_t ldsa_u16(uint32_t a)
+{
+    uint16_t r;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(a));
+    return r;
+}
 __device__ __forceinline__ float ldsa_f32(uint32_t a)
 {
     float r;
@@ -463,14 +469,20 @@ __device__ __forceinline__ void bin_pair_dispatch(const float (&xa)[NDL], const 
 // tile: the 16 KB factor box; meta: its 32 fmeta entries (512 B); bord: its
 // factors' border arrays (fmeta.x is relative to bord) -- all in the TMA slot,
 // given as buffer offsets.  Quad q, documents d0 + 32n (n < NDL), d0 = dbase + lane.
-template <int NDL, bool CODES, bool WIDE, bool FM, class Sink>
+// CSH: code-column shift.  The model compiler bakes column offsets as col * 128; a
+// 64-document tile (2 documents per lane, DPL = 2) lays its columns 64 bytes apart.
+template <int NDL, bool CODES, bool WIDE, bool FM, class Sink, int CSH = 0>
 __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint32_t bord,
                                              const Sink &bins, int q, int dbase, int lane)
 {
     const uint32_t ma_ = sabs(meta) + 64u * q;
-    const uint4 m0 = ldsa_v4u(ma_), m2 = ldsa_v4u(ma_ + 32u);
+    uint4 m0 = ldsa_v4u(ma_), m2 = ldsa_v4u(ma_ + 32u);
     if (((m0.y | m2.y) & 0xfu) == CLS_SKIP) return;  // warp-uniform: no used factor in the quad
-    const uint4 m1 = ldsa_v4u(ma_ + 16u), m3 = ldsa_v4u(ma_ + 48u);
+    uint4 m1 = ldsa_v4u(ma_ + 16u), m3 = ldsa_v4u(ma_ + 48u);
+    if constexpr (CSH != 0) {
+        m0.z >>= CSH; m0.w >>= CSH; m1.z >>= CSH; m1.w >>= CSH;
+        m2.z >>= CSH; m2.w >>= CSH; m3.z >>= CSH; m3.w >>= CSH;
+    }
     const uint32_t d0 = static_cast<uint32_t>(dbase + lane);
     const uint32_t ta = sabs(tile), ba = sabs(bord);
     float x[4][NDL];
@@ -478,9 +490,10 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
     for (int n = 0; n < NDL; ++n) {
         const uint32_t d = d0 + 32u * n;
         float4 v;
-        if constexpr (FM) {  // feature-major box [32 factors][128 docs]: 512-byte rows, lanes = docs
-            const uint32_t r = ta + q * 4 * 512 + d * 4;
-            v = make_float4(ldsa_f32(r), ldsa_f32(r + 512), ldsa_f32(r + 1024), ldsa_f32(r + 1536));
+        if constexpr (FM) {  // feature-major box [32 factors][tile docs]: lanes = docs
+            constexpr uint32_t RB = 512u >> CSH;  // row bytes
+            const uint32_t r = ta + q * 4 * RB + d * 4;
+            v = make_float4(ldsa_f32(r), ldsa_f32(r + RB), ldsa_f32(r + 2 * RB), ldsa_f32(r + 3 * RB));
         } else {   // doc-major box [128 docs][32 factors], 128B-swizzled (d & 7 == lane & 7)
             v = ldsa_v4f(ta + d * 128 + ((q ^ (lane & 7)) << 4));
         }
@@ -517,11 +530,21 @@ __device__ __forceinline__ Lane make_lane(const KParams &, uint32_t bins_abs) { 
 // shifted into the index.  (Moving the address / merge onto the FMA pipe with
 // IMAD.HI was tried: SASS IMAD.HI takes a 64-bit addend, so every merge needs a
 // register-pair set-up and the FMA pipe became the binder.)
-template <int DEPTH>
+// The lane's code word: 4 documents (u32) or, 64-document tiles, 2 (u16, upper bytes
+// 0: their sums stay below 128, so their flags are 0 and never used).
+template <int DPL>
+__device__ __forceinline__ uint32_t code_word(uint32_t a)
+{
+    if constexpr (DPL == 4) return ldsa_u32(a);
+    else return ldsa_u16(a);
+}
+
+template <int DEPTH, int DPL = 4>
 __device__ __forceinline__ void tree_level(uint32_t dsc, const Lane &ln, int l, uint32_t &lo,
                                            uint32_t &hi)
 {
-    const uint32_t w = ldsa_u32(ln.bins + (dsc >> 12));  // col * 128; absolute address
+    // col * 128 (col * 64 for 64-document tiles); absolute address
+    const uint32_t w = code_word<DPL>(ln.bins + (dsc >> (DPL == 4 ? 12 : 13)));
     const uint32_t s = (w + prmt(dsc, 0u, 0x0000u)) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
@@ -530,11 +553,11 @@ __device__ __forceinline__ void tree_level(uint32_t dsc, const Lane &ln, int l, 
 }
 
 // 8-byte descriptors (depth <= 8): {col * 128, (128 - K) replicated in every byte}
-template <int DEPTH>
+template <int DEPTH, int DPL = 4>
 __device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, const Lane &ln, int l,
                                             uint32_t &lo, uint32_t &hi)
 {
-    const uint32_t w = ldsa_u32(ln.bins + col128);
+    const uint32_t w = code_word<DPL>(ln.bins + (DPL == 4 ? col128 : col128 >> 1));
     const uint32_t s = (w + krep) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
@@ -542,7 +565,7 @@ __device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, cons
         hi = (l == 8) ? s : ((hi >> 1) | s);
 }
 
-template <int DEPTH>
+template <int DEPTH, int DPL = 4>
 __device__ __forceinline__ void tree_flags(uint32_t d, const Lane &ln, uint32_t &lo,
                                            uint32_t &hi)
 {
@@ -552,37 +575,37 @@ __device__ __forceinline__ void tree_flags(uint32_t d, const Lane &ln, uint32_t 
 #pragma unroll
         for (int l = 0; l < DEPTH; l += 2) {  // one LDS.128 per two levels
             const uint4 q = lds_v4u(d + l * 8);
-            tree_level8<DEPTH>(q.x, q.y, ln, l, lo, hi);
-            if (l + 1 < DEPTH) tree_level8<DEPTH>(q.z, q.w, ln, l + 1, lo, hi);
+            tree_level8<DEPTH, DPL>(q.x, q.y, ln, l, lo, hi);
+            if (l + 1 < DEPTH) tree_level8<DEPTH, DPL>(q.z, q.w, ln, l + 1, lo, hi);
         }
     } else {
 #pragma unroll
     for (int l = 0; l < DEPTH; l += 4) {
         if (l + 2 < DEPTH) {  // 3 or 4 levels left: one LDS.128 (padding levels unused)
             const uint4 q = lds_v4u(d + l * 4);
-            tree_level<DEPTH>(q.x, ln, l, lo, hi);
-            tree_level<DEPTH>(q.y, ln, l + 1, lo, hi);
-            tree_level<DEPTH>(q.z, ln, l + 2, lo, hi);
-            if (l + 3 < DEPTH) tree_level<DEPTH>(q.w, ln, l + 3, lo, hi);
+            tree_level<DEPTH, DPL>(q.x, ln, l, lo, hi);
+            tree_level<DEPTH, DPL>(q.y, ln, l + 1, lo, hi);
+            tree_level<DEPTH, DPL>(q.z, ln, l + 2, lo, hi);
+            if (l + 3 < DEPTH) tree_level<DEPTH, DPL>(q.w, ln, l + 3, lo, hi);
         } else if (l + 1 < DEPTH) {
             const uint2 q = lds_v2u(d + l * 4);
-            tree_level<DEPTH>(q.x, ln, l, lo, hi);
-            tree_level<DEPTH>(q.y, ln, l + 1, lo, hi);
+            tree_level<DEPTH, DPL>(q.x, ln, l, lo, hi);
+            tree_level<DEPTH, DPL>(q.y, ln, l + 1, lo, hi);
         } else {
-            tree_level<DEPTH>(lds_u32(d + l * 4), ln, l, lo, hi);
+            tree_level<DEPTH, DPL>(lds_u32(d + l * 4), ln, l, lo, hi);
         }
     }
     }
 }
 
 // Complemented leaf index F of the lane's 4 documents.
-template <int DEPTH>
-__device__ __forceinline__ void tree_findex(uint32_t d, const Lane &ln, uint32_t F[4])
+template <int DEPTH, int DPL = 4>
+__device__ __forceinline__ void tree_findex(uint32_t d, const Lane &ln, uint32_t F[DPL])
 {
     uint32_t lo, hi;
-    tree_flags<DEPTH>(d, ln, lo, hi);
+    tree_flags<DEPTH, DPL>(d, ln, lo, hi);
 #pragma unroll
-    for (int n = 0; n < 4; ++n) {
+    for (int n = 0; n < DPL; ++n) {
         if constexpr (DEPTH == 0) {
             F[n] = 0;
         } else if constexpr (DEPTH <= 8) {
@@ -616,29 +639,29 @@ __device__ __forceinline__ uint32_t swz_bank_hi(uint32_t lo, uint32_t h)
 
 // Absolute shared-window addresses of the 4 leaves (tables reversed and
 // bank-swizzled; tb = the table base, absolute and 256-aligned).
-template <int DEPTH>
+template <int DEPTH, int DPL = 4>
 __device__ __forceinline__ void leaf_addrs(uint32_t d, const Lane &ln, uint32_t tb,
-                                           uint32_t a[4])
+                                           uint32_t a[DPL])
 {
     uint32_t lo, hi;
-    tree_flags<DEPTH>(d, ln, lo, hi);
+    tree_flags<DEPTH, DPL>(d, ln, lo, hi);
     if constexpr (DEPTH <= 6) {
         // byte = F << (8-DEPTH); want 4F in the low byte of a 256-aligned base
         if constexpr (DEPTH < 6 && DEPTH > 0) lo >>= (6 - DEPTH);
         // depth 6: byte bit 7 = F bit 5 -> complement F's 5 low bits (byte bits 2..6)
         if constexpr (DEPTH == 6) lo ^= prmt(lo, 0u, 0xBA98u) & 0x7C7C7C7Cu;
 #pragma unroll
-        for (int n = 0; n < 4; ++n) a[n] = prmt(lo, tb, 0x7650u | n);
+        for (int n = 0; n < DPL; ++n) a[n] = prmt(lo, tb, 0x7650u | n);
     } else if constexpr (DEPTH <= 8) {
         if constexpr (DEPTH == 7) lo = (lo >> 1) & 0x7F7F7F7Fu;  // byte = F
         lo = swz_bank_hi(lo, 0u);
 #pragma unroll
-        for (int n = 0; n < 4; ++n) a[n] = tb + (prmt(lo, 0u, 0x4440u | n) << 2);
+        for (int n = 0; n < DPL; ++n) a[n] = tb + (prmt(lo, 0u, 0x4440u | n) << 2);
     } else {
         const uint32_t h = hi >> (16 - DEPTH);
         lo = swz_bank_hi(lo, h);
 #pragma unroll
-        for (int n = 0; n < 4; ++n)
+        for (int n = 0; n < DPL; ++n)
             a[n] = tb + (prmt(lo, h, 0xCC00u | ((4u + n) << 4) | n) << 2);
     }
 }
@@ -647,11 +670,11 @@ __device__ __forceinline__ void leaf_addrs(uint32_t d, const Lane &ln, uint32_t 
 // Per-lane accumulators of the 4 documents: fp32 leaves summed in fp32 (the
 // north_star's path) or, for MatrixNet integer models, u32 leaves summed in u64
 // (exact, order-free).
-template <bool U32>
+template <bool U32, int DPL = 4>
 struct Acc;
-template <>
-struct Acc<false> {
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
+template <int DPL>
+struct Acc<false, DPL> {
+    float v[DPL] = {};
     // x += a, y += b as one packed FADD2 (each lane an IEEE round-to-nearest add: the
     // same results as two FADDs)
     static __device__ __forceinline__ void add2(float &x, float &y, float a, float b)
@@ -662,53 +685,62 @@ struct Acc<false> {
             : "f"(a), "f"(b));
     }
     // leaves at ABSOLUTE shared-window addresses a[n]
-    __device__ __forceinline__ void add4(const uint32_t (&a)[4])
+    __device__ __forceinline__ void add4(const uint32_t (&a)[DPL])
     {
-        const float g0 = ldsa_f32(a[0]), g1 = ldsa_f32(a[1]), g2 = ldsa_f32(a[2]), g3 = ldsa_f32(a[3]);
-        add2(v[0], v[1], g0, g1);
-        add2(v[2], v[3], g2, g3);
+        float g[DPL];
+#pragma unroll
+        for (int n = 0; n < DPL; ++n) g[n] = ldsa_f32(a[n]);
+#pragma unroll
+        for (int n = 0; n < DPL; n += 2) add2(v[n], v[n + 1], g[n], g[n + 1]);
     }
     // Force the accumulators (hence every gather of the chunk) to be complete before
     // what follows, i.e. before the mbarrier arrive that hands the slot back to the
     // producer (ptxas may otherwise sink the FADDs, leaving gathers in flight).
     __device__ __forceinline__ void pin(uint32_t scratch) const
     {
-        // a store predicated on all four accumulators (never taken in practice): the
+        // a store predicated on all accumulators (never taken in practice): the
         // store cannot issue before the FADDs, hence before the gathers returned,
-        // and it is ordered before the (memory) arrive
-        const uint32_t x = __float_as_uint(v[0]) ^ __float_as_uint(v[1]) ^ __float_as_uint(v[2]) ^
-                           __float_as_uint(v[3]);
+        // and it is ordered before the (memory) arrive (DESIGN.md §7)
+        uint32_t x = 0;
+#pragma unroll
+        for (int n = 0; n < DPL; ++n) x ^= __float_as_uint(v[n]);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0x7fc00001;\n\t@p st.shared.u32 [%1], %0;\n\t}"
                      ::"r"(x), "r"(sabs(scratch)) : "memory");
     }
     static constexpr uint32_t kRed = kRedBytes;
-    // reduction buffer [16 groups][tile_docs]: group g's partials of the lane's 4
+    // reduction buffer [16 groups][tile_docs]: group g's partials of the lane's DPL
     // documents (doc0 = the first document's position in the tile)
     __device__ __forceinline__ void to_red(uint32_t red, int g, int doc0, int tile_docs) const
     {
-        sts_v4f(red + (g * tile_docs + doc0) * 4, v[0], v[1], v[2], v[3]);
+        if constexpr (DPL == 4)
+            sts_v4f(red + (g * tile_docs + doc0) * 4, v[0], v[1], v[2], v[3]);
+        else
+            sst<float2>(red + (g * tile_docs + doc0) * 4, make_float2(v[0], v[1]));
     }
 };
-template <>
-struct Acc<true> {
-    unsigned long long v[4] = {0ull, 0ull, 0ull, 0ull};
-    __device__ __forceinline__ void add4(const uint32_t (&a)[4])
+template <int DPL>
+struct Acc<true, DPL> {
+    unsigned long long v[DPL] = {};
+    __device__ __forceinline__ void add4(const uint32_t (&a)[DPL])
     {
 #pragma unroll
-        for (int n = 0; n < 4; ++n) v[n] += ldsa_u32(a[n]);
+        for (int n = 0; n < DPL; ++n) v[n] += ldsa_u32(a[n]);
     }
     __device__ __forceinline__ void pin(uint32_t scratch) const
     {
-        const uint32_t x = static_cast<uint32_t>(v[0] ^ v[1] ^ v[2] ^ v[3]);
+        unsigned long long x = 0;
+#pragma unroll
+        for (int n = 0; n < DPL; ++n) x ^= v[n];
+        const uint32_t y = static_cast<uint32_t>(x);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %0, 0x7fc00001;\n\t@p st.shared.u32 [%1], %0;\n\t}"
-                     ::"r"(x), "r"(sabs(scratch)) : "memory");
+                     ::"r"(y), "r"(sabs(scratch)) : "memory");
     }
     static constexpr uint32_t kRed = 2 * kRedBytes;
     __device__ __forceinline__ void to_red(uint32_t red, int g, int doc0, int tile_docs) const
     {
         const uint32_t a = red + (g * tile_docs + doc0) * 8;
         sst<ulonglong2>(a, make_ulonglong2(v[0], v[1]));
-        sst<ulonglong2>(a + 16, make_ulonglong2(v[2], v[3]));
+        if constexpr (DPL == 4) sst<ulonglong2>(a + 16, make_ulonglong2(v[2], v[3]));
     }
 };
 
@@ -720,51 +752,53 @@ struct Acc<true> {
 #endif
 constexpr int kApplyUnroll = ODF_APPLY_UNROLL;  // trees in flight per warp
 
-template <int DEPTH, bool U32>
+template <int DEPTH, bool U32, int DPL = 4>
 __device__ __forceinline__ void apply_tree(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
-                                           int i, Acc<U32> &acc)
+                                           int i, Acc<U32, DPL> &acc)
 {
     const uint32_t d = chunk + i * desc_stride(DEPTH);
     // absolute address of the table (256-aligned: the buffer is 1024-aligned), so
     // leaf_addrs yields absolute leaf addresses with no base add
     const uint32_t tb = sabs(chunk + desc_bytes + i * table_stride(DEPTH));
-    uint32_t a[4];
-    leaf_addrs<DEPTH>(d, ln, tb, a);
+    uint32_t a[DPL];
+    leaf_addrs<DEPTH, DPL>(d, ln, tb, a);
     acc.add4(a);
 }
 
-template <int DEPTH, bool U32>
+template <int DEPTH, bool U32, int DPL = 4>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
-                                            int warp, int nk, Acc<U32> &acc)
+                                            int warp, int nk, Acc<U32, DPL> &acc)
 {
     // chunks hold nk * 16 trees (the last one padded with zero-answer trees); a
     // multiple of 4 trees per warp runs 4 trees per iteration (warp-uniform choice)
     if (DEPTH <= 6 && (nk & 3) == 0) {
 #pragma unroll 4
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
 #if ODF_UNROLL3
     } else if (DEPTH <= 6 && nk % 3 == 0) {  // e.g. c3: 96-tree chunks, 6 trees per warp
 #pragma unroll 3
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
 #endif
     } else {
 #pragma unroll kApplyUnroll
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
     }
 }
 
 // Fixed-order combine of the 16 group partials of document tid (< tile_docs) and store:
 // score = (((P_0 + P_1) + P_2) + ... + P_15).
+template <int DPL>
 __device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int tid, int64_t doc,
-                                           int tile_docs, Acc<false> *)
+                                           int tile_docs, Acc<false, DPL> *)
 {
     float s = lds_f32(red + tid * 4);
 #pragma unroll
     for (int g = 1; g < kConsumerWarps; ++g) s += lds_f32(red + (g * tile_docs + tid) * 4);
     if (doc < p.n_docs) p.scores[doc] = s;
 }
+template <int DPL>
 __device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int tid, int64_t doc,
-                                           int tile_docs, Acc<true> *)
+                                           int tile_docs, Acc<true, DPL> *)
 {
     unsigned long long r = 0;
 #pragma unroll
@@ -780,14 +814,16 @@ __device__ __forceinline__ void finish_doc(const KParams &p, uint32_t red, int t
 
 // Split factors (> 127 borders) loaded as true bins: column A <- min(bin,127),
 // column B <- max(bin-127, 0).
+template <int DPL = 4>
 __device__ __forceinline__ void expand_splits(const KParams &p, uint32_t bins, int tid, int nthr)
 {
-    for (int k = tid; k < p.n_split * (kTile / 4); k += nthr) {
-        const uint2 sp = p.splits[k / (kTile / 4)];
-        const uint32_t wd = (k % (kTile / 4)) * 4;
-        const uint32_t w = lds_u32(bins + sp.x + wd);
-        sts_u32(bins + sp.x + wd, __vminu4(w, 0x7f7f7f7fu));
-        sts_u32(bins + sp.y + wd, __vsubus4(w, 0x7f7f7f7fu));
+    constexpr int kT = 32 * DPL, CSH = DPL == 4 ? 0 : 1;  // tile documents, column shift
+    for (int k = tid; k < p.n_split * (kT / 4); k += nthr) {
+        const uint2 sp = p.splits[k / (kT / 4)];
+        const uint32_t wd = (k % (kT / 4)) * 4, ca = sp.x >> CSH, cb = sp.y >> CSH;
+        const uint32_t w = lds_u32(bins + ca + wd);
+        sts_u32(bins + ca + wd, __vminu4(w, 0x7f7f7f7fu));
+        sts_u32(bins + cb + wd, __vsubus4(w, 0x7f7f7f7fu));
     }
 }
 
@@ -819,15 +855,19 @@ __device__ __forceinline__ void expand_wide(const KParams &p, uint32_t stage, ui
 // arrays.  Warp w binarizes quad w >> 1 of every box for documents 64 * (w & 1) +
 // lane (+ 32); the codes of half h go to the code block at h * half_stride.  Only
 // the tile's hv halves that hold documents are loaded and binarized.
-template <bool CODES, bool WIDE, bool FM, int H, class Sink>
+template <bool CODES, bool WIDE, bool FM, int H, class Sink, int DPL = 4>
 __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint32_t ring, uint32_t bars,
                                         int n_fjobs, int S, int warp, int lane, uint32_t &slot,
                                         uint32_t &ph, unsigned long long &wait_ns, int hv)
 {
+    // 128-document tiles: warp w covers documents 64 (w & 1) + lane (+32); 64-document
+    // tiles (DPL = 2): 32 (w & 1) + lane, code columns 64 bytes apart
+    constexpr int NDL = DPL / 2, CSH = DPL == 4 ? 0 : 1;
+    constexpr uint32_t kBox = 32u * DPL * kFSub * 4u;  // one TMA box: tile docs x 32 factors
     const int fsub = p.fsub_per_job, n_fchunks = p.n_fchunks;
     const uint32_t slot_bytes = p.slot_bytes, off_meta = p.off_meta, off_bord = p.off_bord,
                    bord_stride = p.bord_stride;
-    const int q = warp >> 1, dbase = (warp & 1) << 6;
+    const int q = warp >> 1, dbase = (warp & 1) * 32 * NDL;
     for (int j = 0; j < n_fjobs; ++j) {
         const uint32_t full = bars + 16u * slot, empty = full + 8u;
         DIAG_T(tw0);
@@ -844,8 +884,9 @@ __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint3
 #endif
         for (int s = 0; s < nsub; ++s) {
             if constexpr (H == 1) {
-                binarize_sub<2, CODES, WIDE, FM>(sb + s * kFSubBytes, sb + off_meta + s * kMetaBytes,
-                                                 sb + off_bord + s * bord_stride, sink, q, dbase, lane);
+                binarize_sub<NDL, CODES, WIDE, FM, Sink, CSH>(sb + s * kBox, sb + off_meta + s * kMetaBytes,
+                                                            sb + off_bord + s * bord_stride, sink, q, dbase,
+                                                            lane);
             } else {
                 for (int h = 0; h < hv; ++h)
                     binarize_sub<2, CODES, WIDE, FM>(sb + (s * H + h) * kFSubBytes, sb + off_meta + s * kMetaBytes,
@@ -886,16 +927,19 @@ __device__ __forceinline__ int valid_halves(int64_t n_docs, int64_t tile)
     return v < H ? static_cast<int>(v) : H;
 }
 
-template <int MODE, int DEPTH, bool U32, bool WIDE, int H = 1>
+template <int MODE, int DEPTH, bool U32, bool WIDE, int H = 1, int DPL = 4>
 __global__ void __launch_bounds__(kThreads, 1)
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
     constexpr bool HAS_A = MODE != MODE_APPLY;
     constexpr bool HAS_B = MODE != MODE_BINARIZE;
-    constexpr int kTileH = kTile * H;            // documents per tile
+    constexpr int kT = 32 * DPL;                 // documents per tile half (128, or 64 for wide-column models)
+    constexpr uint32_t kBox = kT * kFSub * 4u;   // one TMA box: kT docs x 32 factors
+    constexpr int kTileH = kT * H;               // documents per tile
     constexpr int kSlots = kConsumerWarps / H;   // tree slots per half (phase B)
     constexpr bool MIXED = DEPTH == kMixedDepth;  // per-segment depths (NEXT-2)
     static_assert(!MIXED || (H == 1 && U32), "mixed-height models: integer answers, 128-doc tiles");
+    static_assert(DPL == 4 || (DPL == 2 && H == 1 && !WIDE), "64-document tiles: narrow models, one half");
     static_assert(H == 1 || (H == 2 && !WIDE && MODE != MODE_BINARIZE), "halves: fused/apply, narrow");
     if (smem_addr(smem_raw) & 1023u) __trap();  // alignment the TMA swizzle relies on
     const uint32_t base = 0;
@@ -914,7 +958,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ring jobs of phase B: tree chunks (H = 1) or half-chunks of tc / 2 trees (H = 2)
     const int n_bjobs = HAS_B && !MIXED ? p.n_tchunks * H : 0;
     constexpr bool WIDE_BINS = MODE == MODE_BINARIZE && WIDE;
-    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile * (p.wide ? 2u : 1u);
+    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kT * (p.wide ? 2u : 1u);
     const uint32_t bins_dst = (MODE == MODE_APPLY && p.wide) ? base + p.off_stage : bins;
 
     if (threadIdx.x == 0) {
@@ -956,16 +1000,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t sb = ring + slot * p.slot_bytes;
                     uint32_t tx = 0;
                     for (int s = 0; s < nsub; ++s)
-                        tx += kFSubBytes * hv + kMetaBytes + sld<uint2>(bct + 8u * (c0 + s)).y;
+                        tx += kBox * hv + kMetaBytes + sld<uint2>(bct + 8u * (c0 + s)).y;
                     mbar_expect_tx(full, tx);
                     for (int s = 0; s < nsub; ++s) {
                         const int c = c0 + s;
                         for (int h = 0; h < hv; ++h) {
-                            const int row = static_cast<int>(tile * kTileH + h * kTile);
-                            if (p.fm)  // feature-major input (NEXT-4): box (128 docs, 32 factors)
-                                tma_load_2d(sb + (s * H + h) * kFSubBytes, &tmap, row, c * kFSub, full);
+                            const int row = static_cast<int>(tile * kTileH + h * kT);
+                            if (p.fm)  // feature-major input (NEXT-4): box (kT docs, 32 factors)
+                                tma_load_2d(sb + (s * H + h) * kBox, &tmap, row, c * kFSub, full);
                             else
-                                tma_load_2d(sb + (s * H + h) * kFSubBytes, &tmap, c * kFSub, row, full);
+                                tma_load_2d(sb + (s * H + h) * kBox, &tmap, c * kFSub, row, full);
                         }
                         bulk_g2s(sb + p.off_meta + s * kMetaBytes, p.fmeta + c * kFSub, kMetaBytes,
                                  full);
@@ -1015,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ========================= consumer warps =========================
     const int tid = threadIdx.x;
     const int half = H == 1 ? 0 : warp / kSlots, tslot = H == 1 ? warp : warp % kSlots;
-    const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * 4u);  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * DPL);  // absolute (tree_level)
     const uint32_t desc_off = H == 1 ? p.desc_bytes : p.hdesc_bytes;  // tables in a ring slot
     const int nk = H == 1 ? p.tc / kConsumerWarps : p.tc / (2 * kSlots);  // trees per job per warp
     uint32_t slot = 0, ph = 0, bph = 0;
@@ -1041,11 +1085,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase_a<false, true, false, 1>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
             } else {
                 if (p.fm)
-                    phase_a<MODE == MODE_FUSED, WIDE, true, H>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp, lane,
-                                                               slot, ph, waitA, hv);
+                    phase_a<MODE == MODE_FUSED, WIDE, true, H, SmemSink, DPL>(p, SmemSink{bins}, ring, bars, n_fjobs,
+                                                                              S, warp, lane, slot, ph, waitA, hv);
                 else
-                    phase_a<MODE == MODE_FUSED, WIDE, false, H>(p, SmemSink{bins}, ring, bars, n_fjobs, S, warp,
-                                                                lane, slot, ph, waitA, hv);
+                    phase_a<MODE == MODE_FUSED, WIDE, false, H, SmemSink, DPL>(p, SmemSink{bins}, ring, bars, n_fjobs,
+                                                                               S, warp, lane, slot, ph, waitA, hv);
             }
         }
         if (MODE == MODE_BINARIZE) {
@@ -1061,14 +1105,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.wide)
                 expand_wide(p, base + p.off_stage, bins, tid, kConsumerThreads);
             else
-                for (int h = 0; h < hv; ++h) expand_splits(p, bins + h * p.half_stride, tid, kConsumerThreads);
+                for (int h = 0; h < hv; ++h) expand_splits<DPL>(p, bins + h * p.half_stride, tid, kConsumerThreads);
         }
         DIAG_T(t_adone);
         named_bar_consumers();  // all bins of the tile written
         DIAG_T(t_bstart);
 
         // acc: the group of the warp's next tree; acc2 (H = 2): the other group
-        Acc<U32> acc, acc2;
+        Acc<U32, DPL> acc, acc2;
         if constexpr (MIXED) {
             for (int sg = 0; sg < p.n_seg; ++sg) {
                 const int sd = p.seg[sg].depth, snk = p.seg[sg].tc / kConsumerWarps;
@@ -1078,17 +1122,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(full, ph);
                     const uint32_t sb = ring + slot * p.slot_bytes;
                     switch (sd) {  // warp-uniform: one branch per chunk
-                        case 0: apply_chunk<0, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 1: apply_chunk<1, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 2: apply_chunk<2, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 3: apply_chunk<3, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 4: apply_chunk<4, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 5: apply_chunk<5, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 6: apply_chunk<6, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 7: apply_chunk<7, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 8: apply_chunk<8, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        case 9: apply_chunk<9, U32>(sb, sdesc, ln, tslot, snk, acc); break;
-                        default: apply_chunk<10, U32>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 0: apply_chunk<0, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 1: apply_chunk<1, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 2: apply_chunk<2, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 3: apply_chunk<3, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 4: apply_chunk<4, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 5: apply_chunk<5, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 6: apply_chunk<6, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 7: apply_chunk<7, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 8: apply_chunk<8, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        case 9: apply_chunk<9, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
+                        default: apply_chunk<10, U32, DPL>(sb, sdesc, ln, tslot, snk, acc); break;
                     }
                     acc.pin(pin_scratch);
                     __syncwarp();
@@ -1111,12 +1155,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             {
                 if constexpr (MIXED) {
                 } else if constexpr (H == 1) {
-                    apply_chunk<DEPTH, U32>(sb, desc_off, ln, tslot, nk, acc);
+                    apply_chunk<DEPTH, U32, DPL>(sb, desc_off, ln, tslot, nk, acc);
                 } else {
 #pragma unroll 2
                     for (int k = 0; k < nk; ++k) {
-                        apply_tree<DEPTH, U32>(sb, desc_off, ln, tslot + k * kSlots, acc);
-                        const Acc<U32> t = acc;
+                        apply_tree<DEPTH, U32, DPL>(sb, desc_off, ln, tslot + k * kSlots, acc);
+                        const Acc<U32, DPL> t = acc;
                         acc = acc2;
                         acc2 = t;
                     }
@@ -1133,11 +1177,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_consumers();
         // a warp applies an even number of trees per tile (tc is a multiple of 16), so
         // acc holds group tslot and acc2 group tslot + 8 (H = 2)
-        acc.to_red(red, tslot, half * kTile + lane * 4, kTileH);
-        if (H > 1) acc2.to_red(red, tslot + kSlots, half * kTile + lane * 4, kTileH);
+        acc.to_red(red, tslot, half * kT + lane * DPL, kTileH);
+        if (H > 1) acc2.to_red(red, tslot + kSlots, half * kT + lane * DPL, kTileH);
         named_bar_consumers();
         if (tid < kTileH)
-            finish_doc(p, red, tid, tile * kTileH + tid, kTileH, static_cast<Acc<U32> *>(nullptr));
+            finish_doc(p, red, tid, tile * kTileH + tid, kTileH, static_cast<Acc<U32, DPL> *>(nullptr));
         if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
             fence_proxy_async();  // generic writes to the bins region precede the next TMA
         }
@@ -1159,17 +1203,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // K6: leaf-index export and per-document fingerprint (tests).  Same tree_flags
 // as the apply path; bins and descriptors staged in shared memory by plain loads.
 // ---------------------------------------------------------------------------
-template <int DEPTH>
+template <int DEPTH, int DPL = 4>
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_index_kernel(const KParams p, int fingerprint)
 {
+    constexpr int kT = 32 * DPL;  // documents per tile
     if (smem_addr(smem_raw) & 1023u) __trap();
     const uint32_t base = 0;
     const uint32_t bins = base;
-    const uint32_t descs = base + ((static_cast<uint32_t>(p.n_cols) * kTile + 1023u) & ~1023u);
+    const uint32_t descs = base + ((static_cast<uint32_t>(p.n_cols) * kT + 1023u) & ~1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kTile * (p.wide ? 2u : 1u);
-    const int64_t tile = (fingerprint ? 0 : p.doc0 / kTile) + blockIdx.x;
+    const uint32_t tile_bins_bytes = static_cast<uint32_t>(p.n_used) * kT * (p.wide ? 2u : 1u);
+    const int64_t tile = (fingerprint ? 0 : p.doc0 / kT) + blockIdx.x;
     {
         const uint32_t dst = p.wide ? p.off_stage : bins;
         const uint4 *src = reinterpret_cast<const uint4 *>(p.bins_in + tile * tile_bins_bytes);
@@ -1179,14 +1224,15 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (p.wide)
             expand_wide(p, p.off_stage, bins, tid, kConsumerThreads);
         else
-            expand_splits(p, bins, tid, kConsumerThreads);
+            expand_splits<DPL>(p, bins, tid, kConsumerThreads);
         __syncthreads();
     }
-    const Lane ln = make_lane(p, sabs(bins) + lane * 4u);  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_level)
     const int64_t t_lo = fingerprint ? 0 : p.tree0;
     const int64_t t_hi = fingerprint ? p.n_trees : p.tree0 + p.ntree;
-    uint64_t h[4] = {0xcbf29ce484222325ull, 0xcbf29ce484222325ull, 0xcbf29ce484222325ull,
-                     0xcbf29ce484222325ull};
+    uint64_t h[DPL];
+#pragma unroll
+    for (int n = 0; n < DPL; ++n) h[n] = 0xcbf29ce484222325ull;
     for (int64_t c = t_lo / p.tc; c * p.tc < t_hi; ++c) {
         const uint8_t *chunk = p.chunks + static_cast<size_t>(c) * p.chunk_bytes;
         const uint32_t dbytes = static_cast<uint32_t>(p.tc) * desc_stride(DEPTH);
@@ -1197,10 +1243,10 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (fingerprint) {
             if (warp == 0) {
                 for (int i = 0; i < p.tc && c0 + i < p.n_trees; ++i) {
-                    uint32_t F[4];
-                    tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), ln, F);
+                    uint32_t F[DPL];
+                    tree_findex<DEPTH, DPL>(descs + i * desc_stride(DEPTH), ln, F);
 #pragma unroll
-                    for (int n = 0; n < 4; ++n) {
+                    for (int n = 0; n < DPL; ++n) {
                         const uint32_t idx = F[n] ^ ((1u << DEPTH) - 1u);
                         h[n] = (h[n] ^ (idx & 0xffu)) * 0x100000001b3ull;
                         h[n] = (h[n] ^ (idx >> 8)) * 0x100000001b3ull;
@@ -1211,11 +1257,11 @@ __global__ void __launch_bounds__(kConsumerThreads)
             for (int i = warp; i < p.tc; i += kConsumerWarps) {
                 const int64_t t = c0 + i;
                 if (t < p.tree0 || t >= t_hi) continue;
-                uint32_t F[4];
-                tree_findex<DEPTH>(descs + i * desc_stride(DEPTH), ln, F);
+                uint32_t F[DPL];
+                tree_findex<DEPTH, DPL>(descs + i * desc_stride(DEPTH), ln, F);
 #pragma unroll
-                for (int n = 0; n < 4; ++n) {
-                    const int64_t doc = tile * kTile + lane * 4 + n;
+                for (int n = 0; n < DPL; ++n) {
+                    const int64_t doc = tile * kT + lane * DPL + n;
                     if (doc >= p.doc0 && doc < p.doc0 + p.ndoc)
                         p.idx_out[(doc - p.doc0) * p.ntree + (t - p.tree0)] =
                             static_cast<uint16_t>(F[n] ^ ((1u << DEPTH) - 1u));
@@ -1226,8 +1272,8 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     if (fingerprint && warp == 0) {
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-            const int64_t doc = tile * kTile + lane * 4 + n;
+        for (int n = 0; n < DPL; ++n) {
+            const int64_t doc = tile * kT + lane * DPL + n;
             if (doc < p.n_docs) p.fp_out[doc] = h[n];
         }
     }
@@ -1354,18 +1400,19 @@ __global__ void __launch_bounds__(kConsumerThreads)
 {
     const int64_t tile = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint8_t *bt = p.bins_in + tile * static_cast<int64_t>(p.n_used) * kTile * (p.wide ? 2 : 1);
+    const int kT = p.tile_docs;  // the model's bins tile width (128, or 64)
+    const uint8_t *bt = p.bins_in + tile * static_cast<int64_t>(p.n_used) * kT * (p.wide ? 2 : 1);
     const uint16_t *bt16 = reinterpret_cast<const uint16_t *>(bt);
     for (int u = warp; u < p.n_used; u += kConsumerWarps) {
         const uint32_t base = p.bf_base[u], m = p.bf_base[u + 1] - base;
 #pragma unroll 1
-        for (int q = 0; q < kTile / 32; ++q) {
-            const int64_t g = tile * (kTile / 32) + q;  // 32-document group
+        for (int q = 0; q < kT / 32; ++q) {
+            const int64_t g = tile * (kT / 32) + q;  // 32-document group
             if (g * 32 >= p.n_docs) break;
             const bool valid = g * 32 + lane < p.n_docs;  // padding documents: bit 0
             const uint32_t b = !valid ? 0xffffffffu
-                               : p.wide ? bt16[u * kTile + q * 32 + lane]
-                                        : bt[u * kTile + q * 32 + lane];
+                               : p.wide ? bt16[u * kT + q * 32 + lane]
+                                        : bt[u * kT + q * 32 + lane];
             uint32_t *dst = p.words + g * p.k_bin + base;
             for (uint32_t j0 = 0; j0 < m; j0 += 32) {
                 uint32_t mine = 0;

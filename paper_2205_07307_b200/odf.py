@@ -42,7 +42,8 @@ class _Info(ctypes.Structure):
                 ("smem_fused", ctypes.c_int32), ("num_sms", ctypes.c_int32),
                 ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32),
                 ("bins_elem_bytes", ctypes.c_int32), ("max_tile_docs", ctypes.c_int32),
-                ("stages_fused_256", ctypes.c_int32), ("smem_fused_256", ctypes.c_int32)]
+                ("stages_fused_256", ctypes.c_int32), ("smem_fused_256", ctypes.c_int32),
+                ("bins_tile_docs", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
@@ -175,15 +176,16 @@ def _ptr(t):
     return _vp(t.data_ptr()) if t is not None and t.numel() > 0 else _vp(0)
 
 
-def bins_to_canonical(bins: torch.Tensor, n_docs: int, n_used: int, elem_bytes: int = 1) -> torch.Tensor:
-    """Blocked layout [tile][used][128] -> [n_docs][n_used] (a view + copy, no arithmetic).
-    uint8 bins, or (elem_bytes == 2, wide models) uint16 bins returned as int32."""
-    tiles = (n_docs + TILE_DOCS - 1) // TILE_DOCS
-    b = bins[: tiles * n_used * TILE_DOCS * elem_bytes]
+def bins_to_canonical(bins: torch.Tensor, n_docs: int, n_used: int, elem_bytes: int = 1,
+                      tile_docs: int = TILE_DOCS) -> torch.Tensor:
+    """Blocked layout [tile][used][tile_docs] -> [n_docs][n_used] (a view + copy, no
+    arithmetic).  uint8 bins, or (elem_bytes == 2, wide models) uint16 bins as int32."""
+    tiles = (n_docs + tile_docs - 1) // tile_docs
+    b = bins[: tiles * n_used * tile_docs * elem_bytes]
     if elem_bytes == 2:
         b = b.view(torch.int16).to(torch.int32) & 0xFFFF
-    b = b.view(tiles, n_used, TILE_DOCS)
-    return b.permute(0, 2, 1).reshape(tiles * TILE_DOCS, n_used)[:n_docs]
+    b = b.view(tiles, n_used, tile_docs)
+    return b.permute(0, 2, 1).reshape(tiles * tile_docs, n_used)[:n_docs]
 
 
 class Model:
@@ -444,4 +446,5 @@ class Model:
         return out
 
     def canonical_bins(self, bins: torch.Tensor, n_docs: int) -> torch.Tensor:
-        return bins_to_canonical(bins, n_docs, self.n_used, self.info["bins_elem_bytes"])
+        return bins_to_canonical(bins, n_docs, self.n_used, self.info["bins_elem_bytes"],
+                                 self.info["bins_tile_docs"])

@@ -524,6 +524,78 @@ def test_integer_leaves_exact(depth, n_docs, n_trees):
 
 
 # ---------------------------------------------------------------------------
+# Models wider than one 128-document code block (1,950 factors): 64-document
+# tiles in every kernel
+# ---------------------------------------------------------------------------
+def _wide_columns_case(n_docs, depth=6, n_trees=1200, seed=1950):
+    """Every one of F = 1950 factors used (1950+ code columns, ~250 KB for 128
+    documents), factor 7 with 200 distinct thresholds (two code columns), ties."""
+    rng = np.random.default_rng(seed)
+    F = 1950
+    nodes = n_trees * depth
+    fi = np.concatenate([np.arange(F), rng.integers(0, F, nodes - F)]).astype(np.int32)
+    rng.shuffle(fi)
+    thr = (rng.integers(0, 40, nodes) / 10.0 - 2.0).astype(np.float32)
+    pool = np.sort(rng.standard_normal(200).astype(np.float32))
+    hot = np.flatnonzero(fi == 7)
+    extra = rng.choice(np.flatnonzero(fi != 7), 200, replace=False)
+    fi[extra] = 7
+    thr[extra] = pool
+    thr[hot] = pool[rng.integers(0, 200, hot.size)]
+    ld = (F + 3) // 4 * 4
+    x = np.zeros((n_docs, ld), np.float32)
+    x[:, :F] = rng.standard_normal((n_docs, F)).astype(np.float32)
+    x[::5, 7] = pool[rng.integers(0, 200, x[::5, 7].size)]  # ties on the split factor
+    x[1::7, :F] = np.round(x[1::7, :F] * 10) / 10  # ties with the 0.1-grid thresholds
+    lv = rng.normal(0, 0.01, n_trees << depth).astype(np.float32)
+    return synth.ForestCase("wide_cols", x, F, fi, thr, lv, depth, n_trees)
+
+
+@pytest.mark.parametrize("n_docs,depth", [(1, 6), (63, 6), (64, 6), (65, 6), (1000, 6), (4097, 6),
+                                          (777, 8), (300, 3)])
+def test_wide_column_model_64_document_tiles(n_docs, depth):
+    case = _wide_columns_case(n_docs, depth=depth, n_trees=1200 if depth < 8 else 400)
+    m = cuda_model(case)
+    assert m.info["bins_tile_docs"] == 64 and m.info["n_columns"] > 1800, m.info
+    assert m.info["max_tile_docs"] == 64
+    m.close()
+    full_check(case, idx_window=(0, min(n_docs, 70), case.n_trees - 40, 40))
+
+
+def test_wide_column_model_integer_and_latency_path():
+    import torch
+    from paper_2205_07307_b200 import Model, OdfError
+    case = _wide_columns_case(500, n_trees=600)
+    rng = np.random.default_rng(9)
+    lv = rng.integers(0, 2 ** 32, case.n_trees << 6, dtype=np.uint64).astype(np.uint32)
+    m = Model(case.feature_index, case.thresholds, lv, 6, case.n_features, leaf_type="u32")
+    assert m.info["bins_tile_docs"] == 64
+    x = to_dev(case.x)
+    sums, _ = m.score_u64(x)
+    sums2, _ = m.apply_u64(m.binarize(x), 500)
+    want = oracle.score_u64(case.x, case.feature_index, case.thresholds, lv, 6)
+    assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
+    assert np.array_equal(sums2.cpu().numpy().view(np.uint64), want)
+    m.close()
+    # depth 10 at this width: 16-tree chunks of 4 KB tables (66 KB) x 2 ring slots do not
+    # fit next to even a 64-document code block -> ODF_E_UNSUPPORTED, naming the bound
+    deep = _wide_columns_case(10, depth=10, n_trees=32)
+    with pytest.raises(OdfError) as e:
+        cuda_model(deep)
+    assert e.value.status == 2 and "64 documents" in str(e.value)
+    m = cuda_model(case)
+    with pytest.raises(OdfError) as e:  # the latency path keeps 128-document tiles
+        m.score_latency(x, m.latency_workspace(500))
+    assert e.value.status == 2
+    s = m.score(x, tile_docs=0)
+    with pytest.raises(OdfError) as e:
+        m.score(x, tile_docs=256)
+    assert e.value.status == 2
+    torch.cuda.synchronize()
+    m.close()
+
+
+# ---------------------------------------------------------------------------
 # NEXT-2: paper-native mixed-height model import, exact u64 parity
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("pad_heights", [False, True], ids=["per_height", "padded"])
