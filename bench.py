@@ -303,7 +303,13 @@ def run_ours(args):
     import torch.distributed as dist
 
     ws, rank, local = _dist()
-    if ws > 1:
+    # --dist-backend gloo (tests only): the multi-rank code path on a one-GPU box, every
+    # rank on cuda:0 (a functional check of the sharding, collectives and checks; the
+    # timing of such a run means nothing)
+    local = local % max(1, torch.cuda.device_count())
+    if ws > 1 and args.dist_backend == "gloo":
+        dist.init_process_group("gloo")
+    elif ws > 1:
         # NCCL's communicator-init lines (nranks, transports) on stderr, so the one
         # JSON line stays alone on stdout
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -313,9 +319,13 @@ def run_ours(args):
         probe = torch.ones(1, device=torch.device("cuda", local))
         dist.all_reduce(probe)  # creates the communicator now
         if rank == 0:
-            print(f"[bench] NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}: communicator "
-                  f"nranks={dist.get_world_size()} (all-reduce probe = {int(probe.item())})",
-                  file=sys.stderr, flush=True)
+            try:
+                v = torch.cuda.nccl.version()
+                v = ".".join(map(str, v)) if isinstance(v, (tuple, list)) else str(v)
+            except Exception:
+                v = "?"
+            print(f"[bench] NCCL {v}: communicator nranks={dist.get_world_size()} "
+                  f"(all-reduce probe = {int(probe.item())})", file=sys.stderr, flush=True)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import synth
@@ -518,6 +528,8 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=65536)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: tests only (multi-rank code path on one GPU; timings meaningless)")
     args = ap.parse_args()
     if args.config is None:
         args.config = "c4" if args.shard == "trees" else "c3"

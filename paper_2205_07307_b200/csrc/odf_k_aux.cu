@@ -39,6 +39,7 @@ static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide 
 {
     if (tile_docs == 64) {  // 64-document tiles: narrow models, one half
         if (wide || halves != 1) return nullptr;
+        if (mode == MODE_BINARIZE) return kptr_t64_f(MODE_BINARIZE, 0);  // bins: leaf type irrelevant
         return u32 ? kptr_t64_u(mode, depth) : kptr_t64_f(mode, depth);
     }
     if (depth == kMixedDepth)

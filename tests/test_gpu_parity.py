@@ -579,7 +579,7 @@ def test_wide_column_model_integer_and_latency_path():
     m.close()
     # depth 10 at this width: 16-tree chunks of 4 KB tables (66 KB) x 2 ring slots do not
     # fit next to even a 64-document code block -> ODF_E_UNSUPPORTED, naming the bound
-    deep = _wide_columns_case(10, depth=10, n_trees=32)
+    deep = _wide_columns_case(10, depth=10, n_trees=200)
     with pytest.raises(OdfError) as e:
         cuda_model(deep)
     assert e.value.status == 2 and "64 documents" in str(e.value)

@@ -379,3 +379,31 @@ def test_condition_words_ordered_bits():
                 assert bit == int(np.float32(c.x[i, f]) < per[f][j])
             kb += 1
     assert w.shape == (3, int(counts.sum()))
+
+
+def test_o5_invariant_every_condition_of_c2():
+    """SURVEY 8(c) O5 in full on config c2 (BASELINE size): for every document (100,000),
+    every tree (2,000) and level (6), the raw fp32 condition x < thr (numpy's own
+    compare) equals bin <= k from the oracle's bins and border indices -- 1.2e9 checks,
+    one node at a time over all documents."""
+    from concurrent.futures import ThreadPoolExecutor
+    c = synth.make_case("c2")
+    per, flat, counts, offs = oracle.borders(c.feature_index, c.thresholds, c.n_features)
+    n = c.n_docs
+    b = np.empty((n, c.n_features), np.uint16)
+    step = 8192
+
+    def job(r0):  # the oracle's linear-scan bins, in row blocks (ctypes releases the GIL)
+        b[r0:r0 + step] = oracle.bins(c.x[r0:r0 + step], c.n_features, flat, counts, offs)
+
+    with ThreadPoolExecutor(8) as ex:
+        list(ex.map(job, range(0, n, step)))
+    k = oracle.border_index(c.feature_index, c.thresholds, flat, counts, offs)
+    assert np.all(k >= 0)
+    xt = np.ascontiguousarray(c.x[:, :c.n_features].T)   # [feature][doc]
+    bt = np.ascontiguousarray(b.T)
+    bad = 0
+    for node in range(c.feature_index.size):
+        f = c.feature_index[node]
+        bad += int(np.count_nonzero((xt[f] < c.thresholds[node]) != (bt[f] <= k[node])))
+    assert bad == 0
