@@ -57,9 +57,10 @@ typedef enum {
     ODF_E_CUDA = 4         /* CUDA runtime / launch error (message has cudaGetErrorString) */
 } odf_status;
 
-/* Bins are stored in a blocked layout: tiles of ODF_TILE_DOCS documents; tile
- * g holds n_used rows of ODF_TILE_DOCS elements, row u = used feature u
- * (ascending raw feature id), element j = document g*ODF_TILE_DOCS + j.  An
+/* Bins are stored in a blocked layout: tiles of TD = odf_model_info.bins_tile_docs
+ * documents (ODF_TILE_DOCS = 128, or 64 for models whose 128-document code block
+ * does not fit shared memory); tile g holds n_used rows of TD elements, row u =
+ * used feature u (ascending raw feature id), element j = document g*TD + j.  An
  * element is a uint8, or a little-endian uint16 for a wide model
  * (odf_model_info.bins_elem_bytes).  Elements of padding documents (>= n_docs)
  * in the last tile are defined but meaningless.                             */
@@ -85,7 +86,8 @@ ODF_API const char *odf_last_error(void);      /* thread-local; "" when the last
  *                      range / non-finite threshold or leaf;
  *   ODF_E_UNSUPPORTED  a feature with more than ODF_MAX_BORDERS_WIDE distinct
  *                      thresholds, or a model whose per-tile state exceeds the
- *                      227 KB shared-memory budget (message says which);
+ *                      227 KB shared-memory budget even with 64-document tiles
+ *                      (message says which);
  *   ODF_E_NOMEM / ODF_E_CUDA.  Synchronises the device.  *out = NULL on error. */
 ODF_API odf_status odf_load_model(const int32_t *feature_index, const float *thresholds,
                           const float *leaf_values, int32_t depth, int64_t n_trees,
@@ -208,8 +210,9 @@ ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t
  * and at least 2 x num_sms tiles of 256 documents (odf_score: only when its ring
  * still has >= 3 slots, stages_fused_256).  Scores are bit-identical for
  * every tile width (the summation order of DESIGN.md does not depend on it).
- * Errors: as odf_score / odf_apply; ODF_E_INVALID_ARG for another tile_docs;
- * ODF_E_UNSUPPORTED if 256 is requested and max_tile_docs is 128.            */
+ * Models with odf_model_info.bins_tile_docs == 64 run 64-document tiles only
+ * (tile_docs 0 or 64).  Errors: as odf_score / odf_apply; ODF_E_INVALID_ARG for
+ * another tile_docs; ODF_E_UNSUPPORTED for a width the model does not have.   */
 ODF_API odf_status odf_score_tiles(const odf_model *m, const float *d_factors, int64_t n_docs,
                                    int64_t ld, float *d_scores, int32_t tile_docs, void *stream);
 ODF_API odf_status odf_apply_tiles(const odf_model *m, const uint8_t *d_bins, int64_t n_docs,

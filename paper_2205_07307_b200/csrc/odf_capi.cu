@@ -317,6 +317,12 @@ int choose_halves(const odf_model *m, int mode, int64_t n_docs, int32_t tile_doc
 {
     const Plan &p2 = mode == MODE_FUSED ? m->fused2 : m->apply2;
     *st = ODF_OK;
+    if (m->tile_docs != kTile) {  // a 64-document-tile model has that width only
+        if (tile_docs == 0 || tile_docs == m->tile_docs) return 1;
+        *st = fail(tile_docs == kTile || tile_docs == 2 * kTile ? ODF_E_UNSUPPORTED : ODF_E_INVALID_ARG,
+                   "tile_docs = %d: this model runs %d-document tiles only", tile_docs, m->tile_docs);
+        return 0;
+    }
     if (tile_docs == 0) {
         // 256-document tiles halve the forest's L2 -> shared-memory bytes per document
         // but, next to two code blocks, leave fewer ring slots: the tree stream is then

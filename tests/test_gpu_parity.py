@@ -588,9 +588,12 @@ def test_wide_column_model_integer_and_latency_path():
         m.score_latency(x, m.latency_workspace(500))
     assert e.value.status == 2
     s = m.score(x, tile_docs=0)
-    with pytest.raises(OdfError) as e:
-        m.score(x, tile_docs=256)
-    assert e.value.status == 2
+    s64 = m.score(x, tile_docs=64)
+    assert torch.equal(s.view(torch.int32), s64.view(torch.int32))
+    for td, st in ((128, 2), (256, 2), (32, 1)):
+        with pytest.raises(OdfError) as e:
+            m.score(x, tile_docs=td)
+        assert e.value.status == st
     torch.cuda.synchronize()
     m.close()
 
