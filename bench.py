@@ -495,8 +495,14 @@ def run_ours(args):
             line["check"] = check
             line["fused_kernel_ms_rank0"] = kern_ms
         if tb is not None:
+            # binarise-only moves 4*F_used + F_used algorithmic bytes per
+            # document (factors read, uint8 bins written), apply-only F_used + 4
+            hbm, _ = _peaks()
+            nu = info["n_used_features"]
             line["two_stage"] = {"binarize_ms": tb, "apply_ms": ta,
-                                 "docs_per_s": n / ((tb + ta) / 1000.0)}
+                                 "docs_per_s": n / ((tb + ta) / 1000.0),
+                                 "binarize_hbm_frac": n * 5 * nu / (tb / 1e3) / 1e9 / hbm,
+                                 "binarize_alg_bytes_per_doc": 5 * nu}
         if ws == 1 and args.secondary != "none" and args.secondary != args.config:
             del x
             torch.cuda.empty_cache()

@@ -152,7 +152,8 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
     const uint32_t stage = (mode == MODE_APPLY && m.wide)
                                ? align_up(static_cast<uint64_t>(m.n_used) * kTile * 2, 1024) : 0u;
     const uint32_t red_bytes = (m.leaf_u32 ? 2 * kRedBytes : kRedBytes) * static_cast<uint32_t>(halves) * td / kTile;
-    const uint32_t bins_region = ((mode == MODE_BINARIZE) ? bins : std::max(bins, red_bytes)) + stage;
+    // the binarize kernel writes bins straight to HBM: no tile of bins in shared memory
+    const uint32_t bins_region = ((mode == MODE_BINARIZE) ? 0u : std::max(bins, red_bytes)) + stage;
     const uint32_t bars = align_up(160 + 8u * m.n_fchunks, 128);  // barriers, scratch, bchunk copy
     // a factor sub-tile travels as [halves x 16 KB boxes][512 B fmeta][its border arrays]
     const uint32_t box = td * kFSub * 4u;  // one TMA box: td documents x 32 factors
@@ -167,9 +168,9 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
     }
     uint32_t slot;
     int smax;
-    if (mode == MODE_BINARIZE) {
+    if (mode == MODE_BINARIZE) {  // 3 stages: two CTAs per SM (launch bounds), more warps in flight
         slot = align_up(unit, 1024);
-        smax = 6;
+        smax = 3;
     } else if (mode == MODE_APPLY) {
         slot = tree_slot;
         smax = 4;

@@ -265,6 +265,27 @@ struct GmemSink {
         base[off] = static_cast<uint8_t>(v);
     }
 };
+// The binarize kernel (K1) writes each warp's bins straight to the tile's block of
+// the blocked bins layout in HBM (row u = used factor u at offset u * tile docs):
+// 32 lanes store 32 consecutive bytes per instruction; offsets >= limit (the trash
+// column of unused pair slots) are dropped.
+struct GmemBinsSink {
+    uint8_t *base;
+    uint32_t limit;
+    __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
+    {
+        if (off < limit) base[off] = static_cast<uint8_t>(v);
+    }
+};
+struct GmemBinsSink16 {  // wide models: u16 bins
+    uint16_t *base;
+    uint32_t limit;
+    __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
+    {
+        if (off < limit) base[off] = static_cast<uint16_t>(v);
+    }
+};
+
 // u16 true bins of a wide model (binarize kernel): element offsets, 2 bytes each
 struct SmemSink16 {
     uint32_t base;
@@ -928,7 +949,7 @@ __device__ __forceinline__ int valid_halves(int64_t n_docs, int64_t tile)
 }
 
 template <int MODE, int DEPTH, bool U32, bool WIDE, int H = 1, int DPL = 4>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K1: 2 CTAs per SM
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
     constexpr bool HAS_A = MODE != MODE_APPLY;
@@ -1073,17 +1094,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned long long waitB = 0;
 #endif
         DIAG_T(t_start);
-        if (MODE == MODE_BINARIZE && tile != blockIdx.x) {
-            if (tid == 0) bulk_wait_read_all();  // previous tile's bins fully read by TMA store
-            named_bar_consumers();
-        }
-        if (HAS_A) {
+        if constexpr (MODE == MODE_BINARIZE) {  // K1: bins straight to HBM, no shared-memory tile
+            const uint32_t lim = static_cast<uint32_t>(p.n_used) * kT;
             if constexpr (WIDE_BINS) {
+                const GmemBinsSink16 snk{reinterpret_cast<uint16_t *>(p.bins_out + tile * tile_bins_bytes), lim};
                 if (p.fm)
-                    phase_a<false, true, true, 1>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
+                    phase_a<false, true, true, 1>(p, snk, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
                 else
-                    phase_a<false, true, false, 1>(p, SmemSink16{bins}, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
+                    phase_a<false, true, false, 1>(p, snk, ring, bars, n_fjobs, S, warp, lane, slot, ph, waitA, hv);
             } else {
+                const GmemBinsSink snk{p.bins_out + tile * tile_bins_bytes, lim};
+                if (p.fm)
+                    phase_a<false, false, true, 1, GmemBinsSink, DPL>(p, snk, ring, bars, n_fjobs, S, warp, lane,
+                                                                      slot, ph, waitA, hv);
+                else
+                    phase_a<false, false, false, 1, GmemBinsSink, DPL>(p, snk, ring, bars, n_fjobs, S, warp, lane,
+                                                                       slot, ph, waitA, hv);
+            }
+            continue;
+        } else if (HAS_A) {
+            {
                 if (p.fm)
                     phase_a<MODE == MODE_FUSED, WIDE, true, H, SmemSink, DPL>(p, SmemSink{bins}, ring, bars, n_fjobs,
                                                                               S, warp, lane, slot, ph, waitA, hv);
@@ -1091,13 +1121,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase_a<MODE == MODE_FUSED, WIDE, false, H, SmemSink, DPL>(p, SmemSink{bins}, ring, bars, n_fjobs,
                                                                                S, warp, lane, slot, ph, waitA, hv);
             }
-        }
-        if (MODE == MODE_BINARIZE) {
-            fence_proxy_async();  // generic-proxy bin stores -> visible to the TMA store
-            named_bar_consumers();
-            if (tid == 0 && tile_bins_bytes > 0)
-                bulk_s2g(p.bins_out + tile * tile_bins_bytes, bins, tile_bins_bytes);
-            continue;
         }
         if (MODE == MODE_APPLY && tile_bins_bytes > 0) {
             mbar_wait(bins_full, bph);
@@ -1196,7 +1219,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++diag_it;
 #endif
     }
-    if (MODE == MODE_BINARIZE && tid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
