@@ -253,9 +253,16 @@ __device__ __forceinline__ uint32_t neg_npad(const uint4 &m)
 
 // Where the bins / codes of a tile go: shared memory (fused, binarize) or a
 // global [n_cols + 1][128] block (latency path).
+// Every sink also has stn(off, v[NDL]): v[n] at off + 32n (the NDL documents of a lane).
 struct SmemSink {
     uint32_t base;
     __device__ __forceinline__ void st(uint32_t off, uint32_t v) const { sts_u8(base + off, v); }
+    template <int NDL>
+    __device__ __forceinline__ void stn(uint32_t off, const uint32_t (&v)[NDL]) const
+    {
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) sts_u8(base + off + 32u * n, v[n]);
+    }
     __device__ __forceinline__ SmemSink at(uint32_t off) const { return SmemSink{base + off}; }
 };
 struct GmemSink {
@@ -263,6 +270,13 @@ struct GmemSink {
     __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
     {
         base[off] = static_cast<uint8_t>(v);
+    }
+    template <int NDL>
+    __device__ __forceinline__ void stn(uint32_t off, const uint32_t (&v)[NDL]) const
+    {
+        uint8_t *q = base + off;
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) q[32 * n] = static_cast<uint8_t>(v[n]);
     }
 };
 // The binarize kernel (K1) writes each warp's bins straight to the tile's block of
@@ -276,6 +290,17 @@ struct GmemBinsSink {
     {
         if (off < limit) base[off] = static_cast<uint8_t>(v);
     }
+    // one bound test and one 64-bit address per factor; the documents 32 apart are
+    // immediate offsets of the same address
+    template <int NDL>
+    __device__ __forceinline__ void stn(uint32_t off, const uint32_t (&v)[NDL]) const
+    {
+        if (off < limit) {
+            uint8_t *q = base + off;
+#pragma unroll
+            for (int n = 0; n < NDL; ++n) q[32 * n] = static_cast<uint8_t>(v[n]);
+        }
+    }
 };
 struct GmemBinsSink16 {  // wide models: u16 bins
     uint16_t *base;
@@ -283,6 +308,15 @@ struct GmemBinsSink16 {  // wide models: u16 bins
     __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
     {
         if (off < limit) base[off] = static_cast<uint16_t>(v);
+    }
+    template <int NDL>
+    __device__ __forceinline__ void stn(uint32_t off, const uint32_t (&v)[NDL]) const
+    {
+        if (off < limit) {
+            uint16_t *q = base + off;
+#pragma unroll
+            for (int n = 0; n < NDL; ++n) q[32 * n] = static_cast<uint16_t>(v[n]);
+        }
     }
 };
 
@@ -292,6 +326,12 @@ struct SmemSink16 {
     __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
     {
         sst<uint16_t>(base + 2u * off, static_cast<uint16_t>(v));
+    }
+    template <int NDL>
+    __device__ __forceinline__ void stn(uint32_t off, const uint32_t (&v)[NDL]) const
+    {
+#pragma unroll
+        for (int n = 0; n < NDL; ++n) st(off + 32u * n, v[n]);
     }
     __device__ __forceinline__ SmemSink16 at(uint32_t off) const { return SmemSink16{base + off}; }
 };
@@ -314,8 +354,7 @@ __device__ __forceinline__ void store_bins(const Sink &s, const uint4 &m, uint32
             s.st(m.w + d0 + 32 * n, max(bin[n], 127u) - 127u);
         }
     } else {
-#pragma unroll
-        for (int n = 0; n < NDL; ++n) s.st(m.z + d0 + 32 * n, bin[n]);
+        s.template stn<NDL>(m.z + d0, bin);
     }
 }
 
@@ -327,11 +366,8 @@ __device__ __forceinline__ void store_pair(const Sink &s, const uint4 &ma, const
         store_bins<NDL, CODES>(s, ma, d0, ra);
         store_bins<NDL, CODES>(s, mb, d0, rb);
     } else {
-#pragma unroll
-        for (int n = 0; n < NDL; ++n) {
-            s.st(ma.z + d0 + 32 * n, ra[n]);
-            s.st(mb.z + d0 + 32 * n, rb[n]);
-        }
+        s.template stn<NDL>(ma.z + d0, ra);
+        s.template stn<NDL>(mb.z + d0, rb);
     }
 }
 
