@@ -1265,10 +1265,15 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
                     workspace_bytes, off[3]);
     if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0)
         return fail(ODF_E_INVALID_ARG, "workspace not 256-byte aligned");
+    // code columns + 2 (else 1) tree-chunk buffers + reduction buffer + mbarriers
+    const size_t fixed = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) + kRedBytes + 64;
+    const int nbuf = fixed + 2 * align_up(m->chunk_bytes, 1024) <= static_cast<size_t>(m->max_smem) ? 2 : 1;
+    const size_t smem_apply = fixed + nbuf * align_up(m->chunk_bytes, 1024);
     KParams p = base_params(m, m->fused);
     p.n_docs = n_docs;
     p.n_tiles = (n_docs + kTile - 1) / kTile;
     p.scores = d_scores;
+    p.stages = nbuf;
     uint8_t *ws = static_cast<uint8_t *>(d_workspace);
     p.lat_codes = ws + off[0];
     p.lat_partial = reinterpret_cast<float *>(ws + off[1]);
@@ -1281,8 +1286,6 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
         tmp = &tm;
     }
     const size_t smem_bin = kFSubBytes + kMetaBytes + align_up(m->bord_stride, 16) + 64;
-    const size_t smem_apply = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) +
-                              align_up(m->chunk_bytes, 1024) + kRedBytes;
     if (smem_apply > static_cast<size_t>(m->max_smem))
         return fail(ODF_E_UNSUPPORTED, "latency path: %zu B of shared memory > %d", smem_apply, m->max_smem);
     int prev = 0;

@@ -1392,34 +1392,52 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int split = blockIdx.x, S = gridDim.x;
     const int64_t tile = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // shared memory: the tile's code columns, p.stages (1 or 2) tree-chunk buffers, the
+    // reduction buffer, mbarriers [codes, chunk buffer 0, chunk buffer 1]; everything is
+    // staged with bulk copies (cp.async.bulk), not thread loops
     const uint32_t bins = 0;
     const uint32_t cols_bytes = static_cast<uint32_t>(p.n_cols) * kTile;
-    const uint32_t chunk = (cols_bytes + 1023u) & ~1023u;
-    const uint32_t red = chunk + ((p.chunk_bytes + 1023u) & ~1023u);
+    const uint32_t chunk_al = (p.chunk_bytes + 1023u) & ~1023u;
+    const uint32_t chunk0 = (cols_bytes + 1023u) & ~1023u;
+    const int nbuf = p.stages;
+    const uint32_t red = chunk0 + nbuf * chunk_al;
+    const uint32_t bar = red + kRedBytes;
     const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
     const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
-    auto stage_chunk = [&](int c) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.chunks + static_cast<size_t>(c) * p.chunk_bytes);
-        for (uint32_t k = tid; k < p.chunk_bytes / 16; k += kConsumerThreads)
-            sts_v4u(chunk + 16 * k, __ldg(src + k));
+    auto stage_chunk = [&](int c, int b) {  // one thread
+        mbar_expect_tx(bar + 8u + 8u * b, p.chunk_bytes);
+        bulk_g2s(chunk0 + b * chunk_al, p.chunks + static_cast<size_t>(c) * p.chunk_bytes, p.chunk_bytes,
+                 bar + 8u + 8u * b);
     };
-    // the first tree chunk does not depend on kernel (1): stage it before waiting for
-    // that grid (programmatic dependent launch; a plain launch makes the wait a no-op)
-    if (c_lo < c_hi) stage_chunk(c_lo);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.lat_codes + tile * p.code_stride);
-        for (uint32_t k = tid; k < cols_bytes / 16; k += kConsumerThreads) sts_v4u(bins + 16 * k, src[k]);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 8u, 1);
+        mbar_init(bar + 16u, 1);
+        fence_barrier_init();
+        // tree chunks do not depend on kernel (1): start them before waiting for that
+        // grid (programmatic dependent launch; after a plain launch the wait is a no-op)
+        for (int b = 0; b < nbuf && c_lo + b < c_hi; ++b) stage_chunk(c_lo + b, b);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0 && cols_bytes > 0) {  // the codes kernel (1) wrote, now complete and visible
+        mbar_expect_tx(bar, cols_bytes);
+        bulk_g2s(bins, p.lat_codes + tile * p.code_stride, cols_bytes, bar);
+    }
+    __syncthreads();  // barrier initialisation visible to every thread
+    if (cols_bytes > 0) mbar_wait(bar, 0);
     Acc<false> acc;
     const Lane ln = make_lane(p, sabs(bins) + lane * 4u);  // absolute (tree_level)
-    for (int c = c_lo; c < c_hi; ++c) {
-        if (c != c_lo) {
-            __syncthreads();  // previous chunk consumed
-            stage_chunk(c);
+    uint32_t ph0 = 0, ph1 = 0;
+    for (int c = c_lo, i = 0; c < c_hi; ++c, ++i) {
+        const int b = nbuf == 2 ? (i & 1) : 0;
+        mbar_wait(bar + 8u + 8u * b, b ? ph1 : ph0);
+        if (b) ph1 ^= 1u; else ph0 ^= 1u;
+        apply_chunk<DEPTH, false>(chunk0 + b * chunk_al, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
+        if (c + nbuf < c_hi) {  // refill buffer b once every warp's gathers from it are done
+            acc.pin(bar + 24u);
+            __syncthreads();
+            if (tid == 0) stage_chunk(c + nbuf, b);
         }
-        __syncthreads();  // chunk (and, first time, codes) stored
-        apply_chunk<DEPTH, false>(chunk, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
     }
     acc.to_red(red, warp, lane * 4, kTile);
     __syncthreads();
