@@ -2,7 +2,7 @@
 """Benchmark of the oblivious-forest hot path (binarize + apply) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--shard docs|trees]
-                    [--impl ours|reference] [--secondary c2|none]
+                    [--weak] [--impl ours|reference] [--secondary c2|none]
 
 One "step" = one pass of the whole hot path (the fused odf_score kernel:
 binarization + leaf-index assembly + leaf gather/sum) over one
@@ -17,6 +17,8 @@ N > 1 (torchrun, one rank per GPU, NCCL):
       [floor(r*D/N), floor((r+1)*D/N)) with the replicated model and the step
       includes the NCCL all-gather of the scores; rank 0 checks (untimed) that
       the gathered scores are bit-identical to one GPU scoring the whole batch.
+  --weak: every rank scores its own full batch (the same model, its own seeded
+      documents) with no collective on the data path (weak scaling).
   --shard trees (default config c4): rank r holds trees [floor(r*T/N), ...),
       scores every document and the step includes one NCCL reduce (sum) of the
       fp32 partial scores to rank 0; rank 0 checks the tolerance.
@@ -172,7 +174,8 @@ def _config(cfg: str, case, ws: int, shard: str, n_docs_total: int) -> dict:
             "l2": "inputs larger than L2 (%.0f MB > 126 MB); no flush"
                   % (n_docs_total * case.x.shape[1] * 4 / 1e6),
             "parallelism": ("1 GPU" if ws == 1 else f"tree-shard x{ws} + NCCL reduce"
-                            if shard == "trees" else f"doc-shard x{ws} + NCCL all-gather")}
+                            if shard == "trees" else f"doc batches x{ws}, no collective (weak)"
+                            if shard == "weak" else f"doc-shard x{ws} + NCCL all-gather")}
 
 
 def cpu_baseline(case, target_s: float = 10.0):
@@ -208,6 +211,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import synth
+    weak = args.weak and ws > 1 and args.shard == "docs"
     n_docs = synth.CONFIGS[args.config]["n_docs"]
     case = synth.make_case(args.config, rows=(0, min(n_docs, 65536)) if args.config != "c1" else None)
     times = []
@@ -221,9 +225,9 @@ def run_reference(args):
     v = float(np.median(times))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "docs/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v * n_docs,
-            "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong" if ws > 1 and not weak else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(args.config, case, ws, args.shard, n_docs),
+            "config": _config(args.config, case, ws, "weak" if weak else args.shard, n_docs),
             "doc_trees_per_s": v * case.n_trees,
             "cpu_baseline": {"value": v, "unit": "docs/s", "cores": base["cores"],
                              "kind": "oracle", "sample": base["sample"]},
@@ -333,14 +337,18 @@ def run_ours(args):
     from paper_2205_07307_b200.parallel import DocSharded, shard_bounds, tree_shard
 
     tree_mode = args.shard == "trees"
+    weak = args.weak and ws > 1 and not tree_mode  # every rank its own batch, no collective
     D = synth.CONFIGS[args.config]["n_docs"]
-    if tree_mode or ws == 1:
+    if tree_mode or ws == 1 or weak:
         lo, hi = 0, D
     else:
         lo, hi = shard_bounds(D, ws, rank)
     # rank 0 of a doc-sharded run also holds the whole batch for the bit-identity check
-    full_rows = ws == 1 or tree_mode or rank == 0
+    full_rows = ws == 1 or tree_mode or weak or rank == 0
     case = synth.make_case(args.config, rows=None if full_rows else (lo, hi))
+    if weak and rank > 0:  # the same model, rank r's own seeded batch of D documents
+        case.x = synth.ranking_factors(synth.CONFIGS[args.config]["seed"] + 7919 * rank, D,
+                                       case.n_features, ld=case.x.shape[1])
     if tree_mode:
         fi, th, lv, _ = tree_shard(case.feature_index, case.thresholds, case.leaf_values, case.depth,
                                    ws, rank)
@@ -365,7 +373,7 @@ def run_ours(args):
             model.score(x, out=out, stream=stream)
             if ws > 1:  # one NCCL reduce (sum) of the fp32 partial scores to rank 0
                 dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
-        elif ws > 1:  # this rank's documents, then the NCCL all-gather of the scores
+        elif ws > 1 and not weak:  # this rank's documents, then the NCCL all-gather of the scores
             model.score(x, out=loc_pad[:n], stream=stream)
             ds.gather_into(loc_pad, all_pad)
         else:
@@ -384,7 +392,7 @@ def run_ours(args):
 
     # ---- correctness of the sharded result (untimed) ----
     check = None
-    if ws > 1:
+    if ws > 1 and not weak:
         torch.cuda.synchronize()
         if tree_mode:
             step()
@@ -432,13 +440,13 @@ def run_ours(args):
 
     # ---- end to end through the public API from pinned host memory ----
     xh = torch.from_numpy(np.ascontiguousarray(x_host)).pin_memory()
-    if ws > 1 and not tree_mode:
+    if ws > 1 and not tree_mode and not weak:
         sh = torch.empty(m_pad * ws, dtype=torch.float32).pin_memory()
     else:
         sh = torch.empty(n, dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        if ws > 1:  # H2D of this rank's inputs, score, collective, D2H of the result on rank 0
+        if ws > 1 and not weak:  # H2D of this rank's inputs, score, collective, D2H on rank 0
             x.copy_(xh, non_blocking=True)
             step()
             if rank == 0:
@@ -461,29 +469,31 @@ def run_ours(args):
         e2e_s = float(t.item())
     # bytes over all ranks: doc sharding copies each document once, tree sharding every
     # document to every rank; the result read back is the [D] score vector on rank 0
-    h2d = int(D * x_host.shape[1] * 4) * (ws if tree_mode else 1)
-    d2h = int(D * 4)
+    h2d = int(D * x_host.shape[1] * 4) * (ws if tree_mode or weak else 1)
+    d2h = int(D * 4) * (ws if weak else 1)
 
     if rank == 0:
-        docs_total = D * args.steps
+        docs_total = D * args.steps * (ws if weak else 1)
         value = docs_total / (total_ms / 1000.0)
         mhz = clk.summary().get("sm_mhz") or clk.max_mhz
         line = {
             "metric": METRIC, "value": value, "unit": "docs/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong" if ws > 1 and not weak else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": _config(args.config, case, ws, args.shard, D),
+            "config": _config(args.config, case, ws, "weak" if weak else args.shard, D),
             "path": "fused odf_score (one launch per step)" +
                     (" + NCCL reduce" if tree_mode and ws > 1 else
-                     " + NCCL all-gather" if ws > 1 else ""),
+                     " + NCCL all-gather" if ws > 1 and not weak else ""),
             "doc_trees_per_s": value * case.n_trees,
             "roofline": _roofline_hbm(n, info["n_used_features"], kern_ms, args.config),
             "roofline_binding": _roofline_smem(args.config, kern_ms, info["num_sms"], mhz),
-            "e2e": {"value": D * k_e2e / e2e_s, "unit": "docs/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": D * (ws if weak else 1) * k_e2e / e2e_s, "unit": "docs/s",
+                    "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": k_e2e,
                     "path": "odf_score_host (pinned host memory, chunked H2D/score/D2H)"
-                            if ws == 1 else "H2D + odf_score + NCCL collective + D2H on rank 0"},
+                            + (" on every rank" if weak else "")
+                            if ws == 1 or weak else "H2D + odf_score + NCCL collective + D2H on rank 0"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "model": {k: info[k] for k in ("n_split_features", "n_columns", "trees_per_chunk",
@@ -529,6 +539,9 @@ def main():
     ap.add_argument("--shard", default="docs", choices=["docs", "trees"],
                     help="multi-GPU: document sharding of one batch + all-gather, or tree "
                          "sharding + NCCL reduce of fp32 partials (both strong scaling)")
+    ap.add_argument("--weak", action="store_true",
+                    help="multi-GPU: every rank scores its own full batch (same model, its own seed), "
+                         "no collective on the data path (weak scaling)")
     ap.add_argument("--secondary", default="c2", help="second workload reported in the line, or none")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunk", type=int, default=65536)
