@@ -167,12 +167,6 @@ typedef struct {
                                    for models whose 128-document code block does not fit shared
                                    memory (about > 1,600 code columns, e.g. P:168's 1,950 factors;
                                    at depth 9-10 such widths do not fit at all: ODF_E_UNSUPPORTED) */
-    int32_t stages_pipe;        /* pipelined fused kernel (ODF_FUSED_PIPELINED): chunk-ring stages
-                                   with 128-document tiles (0: not available for this model) */
-    int32_t smem_pipe;          /* its dynamic shared memory per CTA, bytes (0: none) */
-    int32_t stages_pipe_256;    /* the same with 256-document tiles (0: none) */
-    int32_t fused_kernel;       /* the model's setting (odf_set_fused_kernel), ODF_FUSED_* */
-    int64_t pipe_scratch_bytes; /* device scratch the pipelined kernel owns (in model_device_bytes) */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);
@@ -204,26 +198,6 @@ ODF_API odf_status odf_apply(const odf_model *m, const uint8_t *d_bins, int64_t 
  * summation order); bins live only in shared memory, never in HBM.           */
 ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
                      float *d_scores, void *stream);
-
-/* Fused kernel (a performance choice, not a numerical one: scores are
- * bit-identical).  ODF_FUSED_SERIAL: every CTA binarizes a tile (all 16 consumer
- * warps), then applies the forest to it, in turn.  ODF_FUSED_PIPELINED: 4 more
- * warps per CTA binarize the NEXT tiles while the 16 apply the forest to the
- * current one; the bins of the next two tiles wait in a per-CTA device scratch
- * the model owns (odf_model_info.pipe_scratch_bytes; it normally stays in L2), so
- * the two phases overlap instead of alternating.  Available for models with
- * uint8 bins, 128-document bins tiles, one height and a fitting shared-memory
- * plan (odf_model_info.stages_pipe > 0), row-major factors only (the _fm
- * variants run SERIAL).  ODF_FUSED_AUTO (the default) takes PIPELINED where
- * available.  Launches of one model on different streams are ordered through
- * its scratch; inside CUDA-graph capture the SERIAL kernel runs (no cross-
- * stream dependency is recorded into the graph).  odf_set_fused_kernel must not
- * run concurrently with a launch on the model.  Errors: ODF_E_INVALID_ARG
- * (unknown value), ODF_E_UNSUPPORTED (PIPELINED on a model without it).       */
-#define ODF_FUSED_AUTO 0
-#define ODF_FUSED_SERIAL 1
-#define ODF_FUSED_PIPELINED 2
-ODF_API odf_status odf_set_fused_kernel(odf_model *m, int32_t kernel);
 
 /* Documents per tile (a performance choice, not a numerical one).  odf_score and
  * odf_apply pick it themselves; these variants take tile_docs = 0 (the same

@@ -84,8 +84,6 @@ struct Plan {
     uint32_t off_stage = 0;  // wide models, apply: u16 bins staging
     size_t smem = 0;
     int grid_per_sm = 1;
-    int bstages = 0;             // MODE_PIPE: border ring
-    uint32_t bslot_bytes = 0, off_bring = 0;
     int halves = 1;              // tile = halves x 128 documents
     uint32_t half_stride = 0;    // bytes between the halves' code blocks
     uint32_t hdesc_bytes = 0;    // halves == 2: tables' offset in a half-chunk ring slot
@@ -127,14 +125,6 @@ struct odf_model {
     double scale = 1.0, bias = 0.0;
     Plan fused, binz, apply;
     Plan fused2, apply2;  // 256-document tiles (two halves), when they fit
-    Plan pipe, pipe2;     // pipelined fused kernel (MODE_PIPE), 128- / 256-document tiles
-    int32_t fused_kernel = ODF_FUSED_AUTO;  // odf_set_fused_kernel
-    // MODE_PIPE scratch: per CTA two tiles of bins; one launch at a time uses it
-    // (launches on different streams are ordered through scratch_ev)
-    uint8_t *d_scratch = nullptr;
-    size_t scratch_bytes = 0;
-    mutable std::mutex scratch_mu;
-    cudaEvent_t scratch_ev = nullptr;
     // odf_score_host staging
     std::mutex host_mu;
     float *d_stage[2] = {nullptr, nullptr};
@@ -213,59 +203,6 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
     pl.off_red = off;                     // reduction buffer aliases the bins (dead by then)
     pl.off_stage = off + bins_region - stage;
     off += bins_region;
-    pl.off_bars = off;
-    off += bars;
-    pl.smem = off;
-    pl.valid = true;
-    return true;
-}
-
-// Pipelined fused kernel (MODE_PIPE): [chunk ring][code block(s)][border ring][bars].
-// At least 2 chunk slots (3 preferred: the tree stream is bound by its bytes in
-// flight) and 2 border slots.  Narrow models, 128-document tiles, one height.
-uint32_t pipe_bslot(const odf_model &m) { return align_up(kMetaBytes + static_cast<uint64_t>(m.bord_stride), 128); }
-bool make_plan_pipe(const odf_model &m, Plan &pl, int halves)
-{
-    pl = Plan();
-    if (m.wide || m.tile_docs != kTile || m.n_seg > 1 || m.n_used == 0 || m.n_fchunks > 2048) return false;
-    if (halves == 2 && (m.leaf_u32 || m.depth < 7)) return false;
-    const uint32_t half_bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * kTile, 1024);
-    const uint32_t bins = half_bins * static_cast<uint32_t>(halves);
-    const uint32_t red_bytes = (m.leaf_u32 ? 2 * kRedBytes : kRedBytes) * static_cast<uint32_t>(halves);
-    const uint32_t bins_region = std::max(bins, red_bytes);
-    uint32_t hdesc = 0, slot;
-    if (halves == 1) {
-        slot = align_up(m.chunk_bytes, 1024);
-    } else {
-        hdesc = align_up(static_cast<uint64_t>(m.tc / 2) * desc_stride(m.depth), 256);
-        slot = align_up(hdesc + static_cast<uint64_t>(m.tc / 2) * m.table_stride, 1024);
-    }
-    const uint32_t bslot = pipe_bslot(m);
-    const uint32_t bars = align_up(kPipeBarBchunk + 8u * m.n_fchunks, 128);
-    const int64_t avail = static_cast<int64_t>(m.max_smem) - 1024 - bins_region - bars;
-    // chunk slots first (3, else 2), then as many border slots as fit (2..4), then a
-    // 4th chunk slot if there is room left
-    int S = 0, SB = 0;
-    for (int s = 3; s >= 2 && !S; --s)
-        if (static_cast<int64_t>(s) * slot + 2 * static_cast<int64_t>(bslot) <= avail) S = s;
-    if (!S) return false;
-    SB = static_cast<int>(std::min<int64_t>(4, (avail - static_cast<int64_t>(S) * slot) / bslot));
-    if (S == 3 && 4 * static_cast<int64_t>(slot) + static_cast<int64_t>(SB) * bslot <= avail) S = 4;
-    pl.halves = halves;
-    pl.half_stride = half_bins;
-    pl.hdesc_bytes = hdesc;
-    pl.slot_bytes = slot;
-    pl.stages = S;
-    pl.bstages = SB;
-    pl.bslot_bytes = bslot;
-    uint32_t off = 0;
-    pl.off_ring = off;
-    off += S * slot;
-    pl.off_bins = pl.off_red = off;
-    off += bins_region;
-    pl.off_bring = off;
-    off += SB * bslot;
-    off = align_up(off, 128);
     pl.off_bars = off;
     off += bars;
     pl.smem = off;
@@ -456,8 +393,6 @@ void odf_free_model(odf_model *m)
         if (m->ev_out[i]) cudaEventDestroy(m->ev_out[i]);
     }
     if (m->ev_in) cudaEventDestroy(m->ev_in);
-    cudaFree(m->d_scratch);
-    if (m->scratch_ev) cudaEventDestroy(m->scratch_ev);
     cudaSetDevice(prev);
     delete m;
 }
@@ -805,13 +740,6 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
     // ring is as deep as shared memory allows (up to 8 stages: more factor data in
     // flight while phase A runs); at least 16 trees (one per consumer warp)
     const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
-    // ... and, for the pipelined fused kernel (make_plan_pipe), small enough that 3
-    // chunk slots fit next to the code block and 2 border slots in 227 KB (the
-    // B200 opt-in limit; the device plan is checked at load)
-    const int64_t pipe_room = (int64_t(227) * 1024 - 1024 -
-                               align_up(static_cast<uint64_t>(m->n_cols + 1) * kTile, 1024) -
-                               2 * static_cast<int64_t>(pipe_bslot(*m)) -
-                               align_up(kPipeBarBchunk + 8u * m->n_fchunks, 128)) / 3;
     std::vector<uint8_t> chunks;
     int64_t total_chunk_bytes = 0;
     for (size_t sg = 0; sg < segs.size(); ++sg) {
@@ -820,9 +748,7 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         const int dstride = desc_stride(sdepth);
         const uint32_t tstride = static_cast<uint32_t>(table_stride(sdepth));
         const uint32_t per = static_cast<uint32_t>(dstride) + tstride;
-        int32_t tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, unit / (16u * per)));
-        const int64_t tc_pipe = pipe_room > 0 ? 16 * ((pipe_room - 256) / (16 * static_cast<int64_t>(per))) : 0;
-        if (segs.size() == 1 && !m->wide && tc_pipe >= 32 && tc_pipe < tc) tc = static_cast<int32_t>(tc_pipe);
+        const int32_t tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, unit / (16u * per)));
         const uint32_t dbytes = align_up(static_cast<uint64_t>(tc) * dstride, 256);
         const uint32_t cbytes = dbytes + static_cast<uint32_t>(tc) * tstride;
         const int32_t nch = static_cast<int32_t>((g.n_trees + tc - 1) / tc);
@@ -969,21 +895,6 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         if (!make_plan(*m, MODE_APPLY, m->apply2, why2, 2)) m->apply2 = Plan();
         if (!m->fused2.valid || !m->apply2.valid) m->fused2 = m->apply2 = Plan();  // both or neither
     }
-    // pipelined fused kernel: plans, and the per-CTA scratch (two tiles of bins)
-    make_plan_pipe(*m, m->pipe, 1);
-    make_plan_pipe(*m, m->pipe2, 2);
-    if (m->pipe.valid || m->pipe2.valid) {
-        const size_t halves = m->pipe2.valid ? 2 : 1;
-        m->scratch_bytes = static_cast<size_t>(m->num_sms) * 2 * halves * m->n_used * kTile;
-        e = cudaMalloc(reinterpret_cast<void **>(&m->d_scratch), m->scratch_bytes);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->scratch_ev, cudaEventDisableTiming);
-        if (e != cudaSuccess) {
-            odf_free_model(m.release());
-            return e == cudaErrorMemoryAllocation ? fail(ODF_E_NOMEM, "device allocation failed")
-                                                  : cuda_fail(e, "pipelined-kernel scratch");
-        }
-        m->dev_bytes += static_cast<int64_t>(m->scratch_bytes);
-    }
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         odf_free_model(m.release());
@@ -1017,11 +928,6 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->bins_elem_bytes = m->wide ? 2 : 1;
     info->max_tile_docs = m->fused2.valid ? 2 * kTile : m->tile_docs;
     info->bins_tile_docs = m->tile_docs;
-    info->stages_pipe = m->pipe.valid ? m->pipe.stages : 0;
-    info->smem_pipe = m->pipe.valid ? static_cast<int32_t>(m->pipe.smem) : 0;
-    info->stages_pipe_256 = m->pipe2.valid ? m->pipe2.stages : 0;
-    info->fused_kernel = m->fused_kernel;
-    info->pipe_scratch_bytes = static_cast<int64_t>(m->scratch_bytes);
     info->stages_fused_256 = m->fused2.valid ? m->fused2.stages : 0;
     info->smem_fused_256 = m->fused2.valid ? static_cast<int32_t>(m->fused2.smem) : 0;
     return ok();
@@ -1070,73 +976,6 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
                                 grid_for(m, pl, p.n_tiles), pl.smem, s, halves);
     if (prev != m->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-    return ok();
-}
-
-// The pipelined fused kernel (odf.h ODF_FUSED_PIPELINED): the tile width it runs for
-// this call (1 or 2 halves), or 0 when the serial kernel runs instead.
-static int pipe_halves(const odf_model *m, int64_t n_docs, int32_t tile_docs, cudaStream_t s)
-{
-    if (m->fused_kernel == ODF_FUSED_SERIAL || !m->d_scratch) return 0;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    if (cs != cudaStreamCaptureStatusNone) return 0;  // graphs: the serial kernel (no scratch dependency)
-    if (tile_docs == 2 * kTile) return m->pipe2.valid ? 2 : 0;
-    if (tile_docs == kTile) return m->pipe.valid ? 1 : 0;
-    if (tile_docs != 0) return 0;
-    // automatic width: as choose_halves (deep forests with enough 256-document tiles)
-    const int64_t tiles256 = (n_docs + 2 * kTile - 1) / (2 * kTile);
-    if (m->pipe2.valid && m->depth >= 7 && tiles256 >= 2 * static_cast<int64_t>(m->num_sms)) return 2;
-    return m->pipe.valid ? 1 : 0;
-}
-
-static odf_status run_pipe(const odf_model *m, int halves, const float *d_x, int64_t n_docs, int64_t ld,
-                           float *scores, cudaStream_t s, uint64_t *sums = nullptr, double *dscores = nullptr)
-{
-    const Plan &pl = halves == 2 ? m->pipe2 : m->pipe;
-    KParams p = base_params(m, pl);
-    p.n_docs = n_docs;
-    p.n_tiles = (n_docs + kTile * halves - 1) / (kTile * halves);
-    p.scores = scores;
-    p.sums = reinterpret_cast<unsigned long long *>(sums);
-    p.dscores = dscores;
-    p.x = d_x;
-    p.ld = ld;
-    p.n_features = m->n_features;
-    p.scratch = m->d_scratch;
-    p.off_bring = pl.off_bring;
-    p.bslot_bytes = pl.bslot_bytes;
-    p.bstages = pl.bstages;
-    CUtensorMap tm;  // the factors' tensor map: L2 prefetch of each job's factors
-    odf_status st = encode_tmap(m, d_x, n_docs, ld, &tm, false);
-    if (st != ODF_OK) return st;
-    const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, m->num_sms));  // scratch: num_sms CTAs
-    int prev = 0;
-    cudaGetDevice(&prev);
-    if (prev != m->device) cudaSetDevice(m->device);
-    cudaError_t e;
-    {
-        std::lock_guard<std::mutex> lk(m->scratch_mu);
-        e = cudaStreamWaitEvent(s, m->scratch_ev, 0);  // the previous user of the scratch
-        if (e == cudaSuccess) e = launch_pipe(m->kdepth, p, &tm, grid, pl.smem, s, halves);
-        if (e == cudaSuccess) e = cudaEventRecord(m->scratch_ev, s);
-    }
-    if (prev != m->device) cudaSetDevice(prev);
-    if (e != cudaSuccess) return cuda_fail(e, "pipelined kernel launch");
-    return ok();
-}
-
-odf_status odf_set_fused_kernel(odf_model *m, int32_t kernel)
-{
-    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
-    if (kernel != ODF_FUSED_AUTO && kernel != ODF_FUSED_SERIAL && kernel != ODF_FUSED_PIPELINED)
-        return fail(ODF_E_INVALID_ARG, "fused kernel %d: not ODF_FUSED_AUTO / _SERIAL / _PIPELINED", kernel);
-    if (kernel == ODF_FUSED_PIPELINED && !m->d_scratch)
-        return fail(ODF_E_UNSUPPORTED, "this model has no pipelined fused kernel (odf_model_info.stages_pipe)");
-    m->fused_kernel = kernel;
     return ok();
 }
 
@@ -1193,8 +1032,6 @@ odf_status odf_score_tiles(const odf_model *m, const float *d_factors, int64_t n
     if (!halves) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
-    if (const int ph = pipe_halves(m, n_docs, tile_docs, static_cast<cudaStream_t>(stream)))
-        return run_pipe(m, ph, d_factors, n_docs, ld, d_scores, static_cast<cudaStream_t>(stream));
     return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, d_scores,
                     static_cast<cudaStream_t>(stream), nullptr, nullptr, false, halves);
 }
@@ -1293,9 +1130,6 @@ odf_status odf_score_u64(const odf_model *m, const float *d_factors, int64_t n_d
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
     if (!d_sums && !d_scores) return fail(ODF_E_INVALID_ARG, "d_sums and d_scores are both NULL");
-    if (const int ph = pipe_halves(m, n_docs, kTile, static_cast<cudaStream_t>(stream)))
-        return run_pipe(m, ph, d_factors, n_docs, ld, nullptr, static_cast<cudaStream_t>(stream), d_sums,
-                        d_scores);
     return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, nullptr,
                     static_cast<cudaStream_t>(stream), d_sums, d_scores);
 }

@@ -11,9 +11,6 @@ constexpr int kTile = 128;                 // documents per tile (4 per lane x 3
 constexpr int kConsumerWarps = 16;         // = number of tree groups
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kThreads = kConsumerThreads + 32;  // + 1 producer (TMA) warp
-constexpr int kPipeBinz = 8;                     // MODE_PIPE: binarizer warps
-constexpr int kPipeThreads = kThreads + kPipeBinz * 32;
-constexpr uint32_t kPipeBarBchunk = 256;         // MODE_PIPE bars: offset of the p.bchunk copy
 constexpr int kFSub = 32;                  // factors per TMA sub-tile (32 x 4 B = 128 B rows)
 constexpr uint32_t kFSubBytes = kTile * kFSub * 4;  // 16 KB TMA box [128 docs x 32 factors]
 constexpr uint32_t kMetaBytes = kFSub * 16;         // fmeta of one sub-tile
@@ -47,7 +44,7 @@ __host__ __device__ constexpr int trees_per_chunk(int depth)
                      : 1);
 }
 
-enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2, MODE_PIPE = 3 };
+enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 
 // Mixed-height models (NEXT-2, the paper's native layout): the forest is a
 // list of height segments, each with its own tree-chunk geometry, concatenated in
@@ -109,13 +106,6 @@ struct KParams {
     uint32_t hdesc_bytes;    // H = 2: offset of the tables in a half-chunk ring slot
     int32_t stages;
     int32_t fsub_per_job;    // factor sub-tiles per job (tiles, then metas, then borders)
-    // ---- pipelined fused kernel (MODE_PIPE) ----
-    const float *x;          // factors, doc-major [n_docs][ld] (plain loads)
-    int64_t ld;
-    int32_t n_features;
-    uint8_t *scratch;        // [grid][2 slots][halves][n_used][128] bins of the next tiles
-    uint32_t off_bring, bslot_bytes;  // border ring: fmeta (512 B) + border arrays per job
-    int32_t bstages;
     // ---- latency path (K4) workspace ----
     uint8_t *lat_codes;      // [n_tiles][n_cols + 1][128] 7-bit codes (+ trash column)
     int64_t code_stride;     // bytes per tile of a global code block: (n_cols + 1) * 128
@@ -148,7 +138,6 @@ const void *kptr_t64_index(int depth);
 const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
 const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);
-const void *kptr_pipe(int depth, bool u32, int halves);  // MODE_PIPE (narrow models, 128-doc tiles)
 
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s, int halves = 1);  // p.tile_docs picks DPL
@@ -161,7 +150,5 @@ cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cu
 cudaError_t prepare_kernels(int max_smem);
 // Number of co-resident CTAs per SM of a main kernel at `smem` bytes.
 int occupancy_main(int mode, int depth, size_t smem, int tile_docs = 128);
-cudaError_t launch_pipe(int depth, const KParams &p, const CUtensorMap *tmap, int grid, size_t smem,
-                        cudaStream_t s, int halves);
 
 }  // namespace odf

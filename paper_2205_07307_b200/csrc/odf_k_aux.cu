@@ -152,13 +152,6 @@ cudaError_t prepare_kernels(int max_smem)
         cudaError_t e = opt_in(main_kernel(MODE_BINARIZE, 0, false, false, 1, 64), max_smem);
         if (e != cudaSuccess) return e;
     }
-    for (int d = 0; d <= 10; ++d)
-        for (int u = 0; u < 2; ++u)
-            for (int h = 1; h <= 2; ++h)
-                if (const void *f = kptr_pipe(d, u != 0, h)) {
-                    cudaError_t e = opt_in(f, max_smem);
-                    if (e != cudaSuccess) return e;
-                }
     cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
     if (e != cudaSuccess) return e;
     e = opt_in(main_kernel(MODE_BINARIZE, 0, false, true), max_smem);

@@ -614,11 +614,7 @@ template <int DEPTH, int DPL = 4>
 __device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, const Lane &ln, int l,
                                             uint32_t &lo, uint32_t &hi)
 {
-#ifndef ODF_HOTLV
-#define ODF_HOTLV 0  // A/B timing probe only (wrong results): levels < ODF_HOTLV skip the code load
-#endif
-    const uint32_t w = (l < ODF_HOTLV) ? (ln.bins ^ col128)
-                                        : code_word<DPL>(ln.bins + (DPL == 4 ? col128 : col128 >> 1));
+    const uint32_t w = code_word<DPL>(ln.bins + (DPL == 4 ? col128 : col128 >> 1));
     const uint32_t s = (w + krep) & 0x80808080u;
     if (l < 8)
         lo = (l == 0) ? s : ((lo >> 1) | s);
@@ -1258,372 +1254,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         }
         ++diag_it;
 #endif
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K3p: the fused path with its two phases on different warps of one CTA
-// (MODE_PIPE).  In odf_main_kernel<MODE_FUSED> all 16 warps binarize a tile
-// (phase A), then apply the forest to it (phase B): the two phases alternate on
-// every SM, and phase A is latency-bound while phase B is bound by the shared-
-// memory data path.  Here kPipeBinz binarizer warps build the bins of the
-// NEXT tiles while the 16 consumer warps apply the forest to the current one:
-//   binarizer warps   factors by plain loads (L2-prefetched by the tensor map),
-//                     borders + fmeta from a small ring of bulk copies, bins
-//                     of tile i into scratch slot i & 1 (global memory, per
-//                     CTA; it stays in L2) -- the binarize kernel's layout;
-//   producer warp     tree chunks into the chunk ring, and each tile's bins
-//                     from its scratch slot into the code block (bulk copy);
-//   consumer warps    exactly the apply kernel's loop (expand, chunks, the
-//                     fixed 16-group reduction, finish_doc).
-// The bins never leave the chip unless L2 evicts the scratch (38 MB at c3 on
-// 148 SMs); the results are bit-identical to MODE_FUSED and MODE_APPLY (same
-// bins, same phase B, same summation order).
-// Shared memory: [chunk ring][code block(s) / reduction][border ring][bars].
-// bars: [0,128) chunk ring full/empty, [128,144) bins_full/empty, [144,160)
-// pin scratch, [160,224) border ring full/empty, [224,240) scratch_full[2],
-// [240,256) scratch_empty[2], [256,...) copy of p.bchunk.
-// ---------------------------------------------------------------------------
-
-// Binarizer output: 4 consecutive documents of a lane -> one u32 store per factor
-// (32 lanes = the 128 bytes of one bins row); offsets >= limit (trash column) dropped.
-struct PackedBinsSink {
-    uint8_t *base;
-    uint32_t limit;
-    __device__ __forceinline__ void st(uint32_t off, uint32_t v) const
-    {
-        if (off < limit) base[off] = static_cast<uint8_t>(v);
-    }
-    template <int NDL>
-    __device__ __forceinline__ void stn(uint32_t off, const uint32_t (&v)[NDL]) const
-    {
-        static_assert(NDL == 4, "packed bins: 4 documents per lane");
-        if (off < limit)
-            *reinterpret_cast<uint32_t *>(base + off) = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
-    }
-};
-
-__device__ __forceinline__ void fence_proxy_async_global()
-{
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1)
-{
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1)
-                 : "memory");
-}
-#ifndef ODF_PIPE_PAIR
-#define ODF_PIPE_PAIR 0
-#endif
-#ifndef ODF_PIPE_LDG
-#define ODF_PIPE_LDG 0  // A/B: 0 no L1 allocation, 1 L1-allocating
-#endif
-__device__ __forceinline__ float4 ldg_v4f(const float *a)
-{
-    float4 r;
-#if ODF_PIPE_LDG == 1
-    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
-#else
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-#endif
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(a));
-    return r;
-}
-
-// One factor quad q of sub-tile c for the lane's 4 documents row0 + 4 lane + n:
-// the factors by plain loads, then the same searches as binarize_sub.
-__device__ __forceinline__ void pipe_quad(const KParams &p, int c, int q, int64_t row0, uint32_t meta,
-                                          uint32_t bord, const PackedBinsSink &snk, int lane)
-{
-    const uint32_t ma_ = sabs(meta) + 64u * q;
-    const uint4 m0 = ldsa_v4u(ma_), m2 = ldsa_v4u(ma_ + 32u);
-    if (((m0.y | m2.y) & 0xfu) == CLS_SKIP) return;  // warp-uniform: no used factor in the quad
-    const uint4 m1 = ldsa_v4u(ma_ + 16u), m3 = ldsa_v4u(ma_ + 48u);
-    const int f0 = c * kFSub + 4 * q;
-    float x[4][4];
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-        const int64_t row = row0 + 4 * lane + n;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-#if ODF_PIPE_DIAG & 1  // diagnostics build only: no factor loads
-        v = make_float4(row * 1e-6f, row * 2e-6f, row * 3e-6f, row * 4e-6f);
-        if (row < 0) {
-#else
-        if (row < p.n_docs) {
-#endif
-            const float *a = p.x + row * p.ld + f0;
-            if (f0 + 4 <= p.n_features) {
-                v = ldg_v4f(a);
-            } else {  // the last sub-tile: factors past n_features are unused (trash column)
-                if (f0 < p.n_features) v.x = a[0];
-                if (f0 + 1 < p.n_features) v.y = a[1];
-                if (f0 + 2 < p.n_features) v.z = a[2];
-            }
-        }
-        x[0][n] = v.x;
-        x[1][n] = v.y;
-        x[2][n] = v.z;
-        x[3][n] = v.w;
-    }
-    const uint32_t ba = sabs(bord), d0 = 4u * lane;
-#if ODF_PIPE_DIAG & 2  // diagnostics build only: no searches
-    {
-        const uint32_t r[4] = {__float_as_uint(x[0][0]) & 1u, __float_as_uint(x[1][1]) & 1u,
-                               __float_as_uint(x[2][2]) & 1u, __float_as_uint(x[3][3]) & 1u};
-        snk.stn<4>(m0.z + d0, r);
-        return;
-    }
-#endif
-    bin_pair_dispatch<4, false, false>(x[0], x[1], m0, m1, ba, snk, d0);
-    bin_pair_dispatch<4, false, false>(x[2], x[3], m2, m3, ba, snk, d0);
-}
-
-#ifndef ODF_PIPE_DIAG
-#define ODF_PIPE_DIAG 0  // diagnostics builds only (tools/): 1 no factor loads, 2 no searches, 4 no phase B
-#endif
-constexpr int kPipePrefetch = 8;
-#if ODF_DIAG & 8  // diagnostics build only: per-tile timeline of the pipelined kernel (tools/pipe_timeline.py)
-#define PIPE_T(li, k)                                                                                     \
-    do {                                                                                                  \
-        if ((li) < kDiagIt && blockIdx.x < 148)                                                           \
-            g_diag[(static_cast<size_t>(blockIdx.x) * kDiagIt + (li)) * 128 + (k)] = gtime();            \
-    } while (0)
-#define PIPE_ADD(li, k, v)                                                                                \
-    do {                                                                                                  \
-        if ((li) < kDiagIt && blockIdx.x < 148)                                                           \
-            g_diag[(static_cast<size_t>(blockIdx.x) * kDiagIt + (li)) * 128 + (k)] += (v);               \
-    } while (0)
-#else
-#define PIPE_T(li, k)
-#define PIPE_ADD(li, k, v)
-#endif  // jobs of factor boxes prefetched into L2 ahead of the loads
-
-template <int DEPTH, bool U32, int H>
-__global__ void __launch_bounds__(kPipeThreads, 1)
-    odf_pipe_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
-{
-    constexpr int kTileH = kTile * H;
-    constexpr int kSlots = kConsumerWarps / H;
-    if (smem_addr(smem_raw) & 1023u) __trap();
-    const uint32_t bins = p.off_bins, ring = p.off_ring, red = p.off_red, bars = p.off_bars;
-    const uint32_t bring = p.off_bring;
-    const int S = p.stages, SB = p.bstages, n_fc = p.n_fchunks;
-    const uint32_t bins_full = bars + 128u, bins_empty = bins_full + 8u;
-    const uint32_t pin_scratch = bars + 144u;
-    const uint32_t bbars = bars + 160u;          // border ring full/empty
-    const uint32_t scr_full = bars + 224u;       // [2]
-    const uint32_t scr_empty = bars + 240u;      // [2]
-    const uint32_t bct = bars + kPipeBarBchunk;  // copy of p.bchunk
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_bjobs = p.n_tchunks * H;
-    const uint32_t tbb = static_cast<uint32_t>(p.n_used) * kTile;  // bins bytes of one tile half
-    const int64_t n_local = (p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    uint8_t *const scratch = p.scratch + static_cast<size_t>(blockIdx.x) * 2u * H * tbb;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(bars + 16u * s, 1);
-            mbar_init(bars + 16u * s + 8u, kConsumerWarps);
-        }
-        for (int s = 0; s < SB; ++s) {
-            mbar_init(bbars + 16u * s, 1);
-            mbar_init(bbars + 16u * s + 8u, kPipeBinz);
-        }
-        mbar_init(bins_full, 1);
-        mbar_init(bins_empty, kConsumerWarps);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(scr_full + 8u * s, kPipeBinz);
-            mbar_init(scr_empty + 8u * s, 1);
-        }
-        fence_barrier_init();
-    }
-    for (int c = threadIdx.x; c < n_fc; c += blockDim.x) sst<uint2>(bct + 8u * c, p.bchunk[c]);
-    __syncthreads();
-
-    if (warp == kConsumerWarps) {
-        // ===================== producer: tree chunks and bins tiles =====================
-        if (lane == 0) {
-            uint32_t slot = 0, ph = 0, bph = 0;
-            auto chunk = [&](int c) {
-                const uint32_t full = bars + 16u * slot, empty = full + 8u;
-                mbar_wait(empty, ph ^ 1u);
-                const uint32_t sb = ring + slot * p.slot_bytes;
-                if constexpr (H == 1) {
-                    mbar_expect_tx(full, p.chunk_bytes);
-                    bulk_g2s(sb, p.chunks + static_cast<size_t>(c) * p.chunk_bytes, p.chunk_bytes, full);
-                } else {
-                    const int half_tc = p.tc / 2;
-                    const uint8_t *ch = p.chunks + static_cast<size_t>(c >> 1) * p.chunk_bytes;
-                    const uint32_t db = static_cast<uint32_t>(half_tc * desc_stride(DEPTH));
-                    const uint32_t tbytes = static_cast<uint32_t>(half_tc * table_stride(DEPTH));
-                    mbar_expect_tx(full, db + tbytes);
-                    bulk_g2s(sb, ch + (c & 1) * db, db, full);
-                    bulk_g2s(sb + p.hdesc_bytes, ch + p.desc_bytes + (c & 1) * tbytes, tbytes, full);
-                }
-                if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
-            };
-            for (int64_t li = 0; li < n_local; ++li) {
-                const int64_t tile = blockIdx.x + li * gridDim.x;
-                const int hv = valid_halves<H>(p.n_docs, tile);
-                const uint32_t s = static_cast<uint32_t>(li & 1);
-                // the tile's first chunks only need ring slots, not its bins
-                const int pre = min(S, n_bjobs);
-                int c = 0;
-                PIPE_T(li, 7);
-                for (; c < pre; ++c) chunk(c);
-                mbar_wait(scr_full + 8u * s, static_cast<uint32_t>((li >> 1) & 1));
-                PIPE_T(li, 5);
-                mbar_wait(bins_empty, bph ^ 1u);
-                mbar_expect_tx(bins_full, tbb * hv);
-                for (int h = 0; h < hv; ++h)
-                    bulk_g2s(bins + h * p.half_stride, scratch + (s * H + h) * tbb, tbb, bins_full);
-                mbar_wait(bins_full, bph);  // landed: the scratch slot is free again
-                PIPE_T(li, 6);
-                mbar_arrive(scr_empty + 8u * s);
-                bph ^= 1u;
-                for (; c < n_bjobs; ++c) chunk(c);
-            }
-        }
-        return;
-    }
-
-    if (warp > kConsumerWarps) {
-        // ===================== binarizer warps =====================
-        const int b = warp - kConsumerWarps - 1;
-        const int64_t n_jobs = n_local * n_fc;
-        // job j = (local tile j / n_fc, factor sub-tile j % n_fc): its fmeta + border
-        // arrays into border-ring slot j % SB; binarizer 0 issues job j + SB - 1 before
-        // it takes job j (slot (j - 1) % SB, freed once every binarizer is done with job j - 1)
-        auto issue = [&](int64_t j) {
-            const uint32_t sl = static_cast<uint32_t>(j % SB);
-            const uint32_t full = bbars + 16u * sl, empty = full + 8u;
-            mbar_wait(empty, static_cast<uint32_t>(((j / SB) & 1) ^ 1));
-            const int c = static_cast<int>(j % n_fc);
-            const uint2 bc = sld<uint2>(bct + 8u * c);
-            const uint32_t sb = bring + sl * p.bslot_bytes;
-            mbar_expect_tx(full, kMetaBytes + bc.y);
-            bulk_g2s(sb, p.fmeta + c * kFSub, kMetaBytes, full);
-            if (bc.y) bulk_g2s(sb + kMetaBytes, reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, full);
-        };
-        // the factors of job j into L2 kPipePrefetch jobs ahead of the binarizers' loads
-        auto prefetch = [&](int64_t j) {
-            const int c = static_cast<int>(j % n_fc);
-            const int64_t tile = blockIdx.x + (j / n_fc) * gridDim.x;
-            const int hv = valid_halves<H>(p.n_docs, tile);
-            for (int h = 0; h < hv; ++h) tma_prefetch_2d(&tmap, c * kFSub, static_cast<int>(tile * kTileH + h * kTile));
-        };
-        if (b == 0 && lane == 0) {
-            for (int64_t j = 0; j < kPipePrefetch && j < n_jobs; ++j) prefetch(j);
-            for (int64_t j = 0; j < SB - 1 && j < n_jobs; ++j) issue(j);
-        }
-        int64_t j = 0;
-        for (int64_t li = 0; li < n_local; ++li) {
-            const int64_t tile = blockIdx.x + li * gridDim.x;
-            const int hv = valid_halves<H>(p.n_docs, tile);
-            const uint32_t s = static_cast<uint32_t>(li & 1);
-            mbar_wait(scr_empty + 8u * s, static_cast<uint32_t>(((li >> 1) & 1) ^ 1));
-            if (b == 0 && lane == 0) PIPE_T(li, 3);
-            for (int c = 0; c < n_fc; ++c, ++j) {
-                if (b == 0 && lane == 0) {
-#if ODF_DIAG & 8
-                    const unsigned long long t0 = gtime();
-#endif
-                    if (j + kPipePrefetch < n_jobs) prefetch(j + kPipePrefetch);
-                    if (j + SB - 1 < n_jobs) issue(j + SB - 1);
-#if ODF_DIAG & 8
-                    PIPE_ADD(li, 9, gtime() - t0);
-#endif
-                }
-                __syncwarp();
-                const uint32_t sl = static_cast<uint32_t>(j % SB);
-                const uint32_t full = bbars + 16u * sl, empty = full + 8u;
-#if ODF_DIAG & 8
-                const unsigned long long tw = gtime();
-#endif
-                mbar_wait(full, static_cast<uint32_t>((j / SB) & 1));
-#if ODF_DIAG & 8
-                if (b == 0 && lane == 0) PIPE_ADD(li, 8, gtime() - tw);
-                if (b == 1 && lane == 0) PIPE_ADD(li, 10, gtime() - tw);
-#endif
-                const uint32_t meta = bring + sl * p.bslot_bytes;
-#if ODF_PIPE_PAIR  // A/B: a warp takes both quads of a 32-byte sector
-                for (int u = b; u < 4 * hv; u += kPipeBinz) {
-                    const int h = u >> 2, q = (u & 3) * 2;
-                    const PackedBinsSink snk{scratch + (s * H + h) * tbb, tbb};
-                    pipe_quad(p, c, q, tile * kTileH + h * kTile, meta, meta + kMetaBytes, snk, lane);
-                    pipe_quad(p, c, q + 1, tile * kTileH + h * kTile, meta, meta + kMetaBytes, snk, lane);
-                }
-#else
-                for (int u = b; u < 8 * hv; u += kPipeBinz) {
-                    const int h = u >> 3, q = u & 7;
-                    const PackedBinsSink snk{scratch + (s * H + h) * tbb, tbb};
-                    pipe_quad(p, c, q, tile * kTileH + h * kTile, meta, meta + kMetaBytes, snk, lane);
-                }
-#endif
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty);
-            }
-            fence_proxy_async_global();  // the bins stores precede the producer's bulk copy
-            __syncwarp();
-            if (b == 0 && lane == 0) PIPE_T(li, 4);
-            if (lane == 0) mbar_arrive(scr_full + 8u * s);
-        }
-        return;
-    }
-
-    // ========================= consumer warps (the apply loop) =========================
-    const int tid = threadIdx.x;
-    const int half = H == 1 ? 0 : warp / kSlots, tslot = H == 1 ? warp : warp % kSlots;
-    const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * 4);
-    const uint32_t desc_off = H == 1 ? p.desc_bytes : p.hdesc_bytes;
-    const int nk = H == 1 ? p.tc / kConsumerWarps : p.tc / (2 * kSlots);
-    uint32_t slot = 0, ph = 0, bph = 0;
-    for (int64_t li = 0; li < n_local; ++li) {
-        const int64_t tile = blockIdx.x + li * gridDim.x;
-        const int hv = valid_halves<H>(p.n_docs, tile);
-        mbar_wait(bins_full, bph);
-        if (tid == 0) PIPE_T(li, 0);
-        bph ^= 1u;
-        for (int h = 0; h < hv; ++h) expand_splits<4>(p, bins + h * p.half_stride, tid, kConsumerThreads);
-        named_bar_consumers();
-        Acc<U32, 4> acc, acc2;
-        for (int c = 0; c < n_bjobs; ++c) {
-            const uint32_t full = bars + 16u * slot, empty = full + 8u;
-            mbar_wait(full, ph);
-            const uint32_t sb = ring + slot * p.slot_bytes;
-#if ODF_PIPE_DIAG & 4  // diagnostics build only: no phase B
-            if (n_bjobs < 0)
-#endif
-            if constexpr (H == 1) {
-                apply_chunk<DEPTH, U32, 4>(sb, desc_off, ln, tslot, nk, acc);
-            } else {
-#pragma unroll 2
-                for (int k = 0; k < nk; ++k) {
-                    apply_tree<DEPTH, U32, 4>(sb, desc_off, ln, tslot + k * kSlots, acc);
-                    const Acc<U32, 4> t = acc;
-                    acc = acc2;
-                    acc2 = t;
-                }
-            }
-            acc.pin(pin_scratch);
-            if (H > 1) acc2.pin(pin_scratch);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty);
-            if (++slot == static_cast<uint32_t>(S)) { slot = 0; ph ^= 1u; }
-        }
-        if (tid == 0) PIPE_T(li, 1);
-        named_bar_consumers();  // the reduction buffer aliases the bins
-        acc.to_red(red, tslot, half * kTile + lane * 4, kTileH);
-        if (H > 1) acc2.to_red(red, tslot + kSlots, half * kTile + lane * 4, kTileH);
-        named_bar_consumers();
-        if (tid < kTileH) finish_doc(p, red, tid, tile * kTileH + tid, kTileH, static_cast<Acc<U32, 4> *>(nullptr));
-        fence_proxy_async();  // generic writes to the code block precede the next bulk copy
-        named_bar_consumers();
-        if (tid == 0) PIPE_T(li, 2);
-        if (lane == 0) mbar_arrive(bins_empty);
     }
 }
 

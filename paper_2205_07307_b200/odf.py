@@ -43,12 +43,7 @@ class _Info(ctypes.Structure):
                 ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32),
                 ("bins_elem_bytes", ctypes.c_int32), ("max_tile_docs", ctypes.c_int32),
                 ("stages_fused_256", ctypes.c_int32), ("smem_fused_256", ctypes.c_int32),
-                ("bins_tile_docs", ctypes.c_int32), ("stages_pipe", ctypes.c_int32),
-                ("smem_pipe", ctypes.c_int32), ("stages_pipe_256", ctypes.c_int32),
-                ("fused_kernel", ctypes.c_int32), ("pipe_scratch_bytes", ctypes.c_int64)]
-
-# odf.h ODF_FUSED_*: which fused kernel odf_score runs (scores are bit-identical)
-FUSED_KERNELS = {"auto": 0, "serial": 1, "pipelined": 2}
+                ("bins_tile_docs", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
@@ -140,8 +135,6 @@ def lib():
     L.odf_score.restype = ctypes.c_int
     L.odf_score.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
     L.odf_score_tiles.restype = ctypes.c_int
-    L.odf_set_fused_kernel.argtypes = [_vp, _i32]
-    L.odf_set_fused_kernel.restype = ctypes.c_int
     L.odf_score_tiles.argtypes = [_vp, _vp, _i64, _i64, _vp, _i32, _vp]
     L.odf_apply_tiles.restype = ctypes.c_int
     L.odf_apply_tiles.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp]
@@ -276,13 +269,6 @@ class Model:
 
     def __exit__(self, *a):
         self.close()
-
-    def set_fused_kernel(self, kernel: str):
-        """odf_set_fused_kernel: "auto" (default), "serial" or "pipelined" (odf.h)."""
-        if kernel not in FUSED_KERNELS:
-            raise ValueError(f"fused kernel {kernel!r}: one of {sorted(FUSED_KERNELS)}")
-        _check(lib().odf_set_fused_kernel(self._h, FUSED_KERNELS[kernel]))
-        self.info["fused_kernel"] = FUSED_KERNELS[kernel]
 
     # -- helpers ----------------------------------------------------------
     def _dev(self):

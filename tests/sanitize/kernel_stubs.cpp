@@ -17,8 +17,4 @@ cudaError_t launch_latency(int, const KParams &, const CUtensorMap *, int, size_
     return cudaErrorNotSupported;
 }
 cudaError_t launch_bits(int, const KParams &, bool, size_t, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t launch_pipe(int, const KParams &, const CUtensorMap *, int, size_t, cudaStream_t, int)
-{
-    return cudaErrorNotSupported;
-}
 }  // namespace odf
