@@ -414,16 +414,27 @@ class Model:
     def score_host(self, x, out=None, chunk_docs: int = 65536, stream=None):
         """End-to-end from host memory (numpy array or CPU tensor, ideally pinned)."""
         if isinstance(x, torch.Tensor):
-            assert x.device.type == "cpu" and x.dtype == torch.float32 and x.stride(1) == 1
+            if not (x.device.type == "cpu" and x.dtype == torch.float32 and x.dim() == 2
+                    and x.stride(1) == 1):
+                raise OdfError(1, "host factors must be a CPU float32 [n_docs, ld] tensor with "
+                                  "unit column stride")
             n, ld, xp = x.shape[0], x.stride(0), x.data_ptr()
             if out is None:
                 out = torch.empty(n, dtype=torch.float32, pin_memory=x.is_pinned())
+            if not (isinstance(out, torch.Tensor) and out.device.type == "cpu"
+                    and out.dtype == torch.float32 and out.is_contiguous() and out.numel() >= n):
+                raise OdfError(1, f"out must be a contiguous CPU float32 tensor with >= {n} elements")
             op = out.data_ptr()
         else:
             x = np.ascontiguousarray(x, dtype=np.float32)
+            if x.ndim != 2:
+                raise OdfError(1, "host factors must be a 2-D [n_docs, n_features] array")
             n, ld, xp = x.shape[0], x.shape[1], x.ctypes.data
             if out is None:
                 out = np.empty(n, np.float32)
+            if not (isinstance(out, np.ndarray) and out.dtype == np.float32
+                    and out.flags["C_CONTIGUOUS"] and out.size >= n):
+                raise OdfError(1, f"out must be a contiguous float32 array with >= {n} elements")
             op = out.ctypes.data
         _check(lib().odf_score_host(self._h, _vp(xp), n, ld, _vp(op), int(chunk_docs),
                                     _stream(stream, self._dev())))

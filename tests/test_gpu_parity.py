@@ -223,6 +223,13 @@ def test_score_host_e2e_matches_device():
     assert np.array_equal(host.numpy().view(np.uint32), dev.view(np.uint32))
     host2 = m.score_host(case.x, chunk_docs=1 << 20)
     assert np.array_equal(host2.view(np.uint32), dev.view(np.uint32))
+    # caller-supplied outputs are checked before any copy is queued
+    from paper_2205_07307_b200 import OdfError
+    for bad in (np.empty(100, np.float32), np.empty(20000, np.float64)):
+        with pytest.raises(OdfError):
+            m.score_host(case.x, out=bad)
+    with pytest.raises(OdfError):
+        m.score_host(xh, out=torch.empty(10, dtype=torch.float32))
     m.close()
 
 
