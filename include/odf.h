@@ -272,15 +272,17 @@ ODF_API odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bi
 
 /* Small-batch latency path (K4, config c5): the same scores as odf_score within
  * the tolerance (the tree sum is split into `splits` contiguous chunk ranges per
- * 128-document tile and combined in ascending split order: deterministic, but a
+ * tile of odf_model_info.bins_tile_docs documents (128, or 64 for wide-column
+ * models) and combined in ascending split order: deterministic, but a
  * different association than odf_score).  Two kernel
  * launches: binarization spread over one CTA per (tile, 32-factor sub-tile), then
  * the apply spread over `splits` CTAs per tile.  splits <= 0 picks a default
  * (about 2 CTAs per SM).  d_workspace: device memory of at least
  * odf_latency_workspace_bytes(m, n_docs, splits) bytes (same `splits`), owned by
  * the caller; concurrent calls need distinct workspaces.  Same argument rules as
- * odf_score, and n_docs <= 65535 x 128 (ODF_E_INVALID_ARG above: tiles are a grid
- * dimension; this is the small-batch path).  Capturable in a CUDA graph (two
+ * odf_score, and n_docs <= 65535 x bins_tile_docs (ODF_E_INVALID_ARG above: tiles
+ * are a grid dimension; this is the small-batch path).  fp32-leaf models only
+ * (ODF_E_UNSUPPORTED for u32 leaves).  Capturable in a CUDA graph (two
  * kernel nodes; the factor pointer is baked into the captured tensor map, so a
  * graph serves one input buffer, tests/test_gpu_parity.py::test_latency_graph). */
 ODF_API size_t odf_latency_workspace_bytes(const odf_model *m, int64_t n_docs, int32_t splits);

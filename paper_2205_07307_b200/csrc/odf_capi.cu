@@ -260,7 +260,7 @@ KParams base_params(const odf_model *m, const Plan &pl)
     p.off_stage = pl.off_stage;
     p.n_used = m->n_used;
     p.n_cols = m->n_cols;
-    p.code_stride = static_cast<int64_t>(m->n_cols + 1) * kTile;
+    p.code_stride = static_cast<int64_t>(m->n_cols + 1) * m->tile_docs;  // K4 code block per tile
     p.tile_docs = m->tile_docs;
     p.off_bins = pl.off_bins;
     p.off_ring = pl.off_ring;
@@ -1218,7 +1218,8 @@ odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bins, int6
 
 static int lat_splits(const odf_model *m, int64_t n_docs, int32_t splits)
 {
-    const int64_t tiles = std::max<int64_t>(1, (n_docs + kTile - 1) / kTile);
+    const int64_t td = m->tile_docs;
+    const int64_t tiles = std::max<int64_t>(1, (n_docs + td - 1) / td);
     int64_t sp = splits > 0 ? splits : (2 * static_cast<int64_t>(m->num_sms)) / tiles;
     sp = std::max<int64_t>(1, std::min<int64_t>(sp, std::max(1, m->n_tchunks)));
     return static_cast<int>(std::min<int64_t>(sp, 1024));
@@ -1226,11 +1227,12 @@ static int lat_splits(const odf_model *m, int64_t n_docs, int32_t splits)
 
 static void lat_layout(const odf_model *m, int64_t n_docs, int sp, size_t off[4])
 {
-    const int64_t tiles = (n_docs + kTile - 1) / kTile;
+    const int64_t td = m->tile_docs;  // documents per tile: 128, or 64 (wide-column models)
+    const int64_t tiles = (n_docs + td - 1) / td;
     auto a256 = [](size_t v) { return (v + 255) / 256 * 256; };
     off[0] = 0;
-    off[1] = a256(static_cast<size_t>(tiles) * (m->n_cols + 1) * kTile);
-    off[2] = off[1] + a256(static_cast<size_t>(tiles) * sp * kTile * 4);
+    off[1] = a256(static_cast<size_t>(tiles) * (m->n_cols + 1) * td);
+    off[2] = off[1] + a256(static_cast<size_t>(tiles) * sp * td * 4);
     off[3] = off[2] + a256(static_cast<size_t>(tiles) * 4);
 }
 
@@ -1252,11 +1254,9 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
-    if (m->tile_docs != kTile)
-        return fail(ODF_E_UNSUPPORTED, "latency path: 128-document tiles only (this model uses %d)",
-                    m->tile_docs);
-    if ((n_docs + kTile - 1) / kTile > 65535)  // tiles are the grid's y dimension
-        return fail(ODF_E_INVALID_ARG, "latency path: n_docs > 65535 x 128 (use odf_score)");
+    const int64_t td = m->tile_docs;  // 128, or 64 for wide-column models
+    if ((n_docs + td - 1) / td > 65535)  // tiles are the grid's y dimension
+        return fail(ODF_E_INVALID_ARG, "latency path: n_docs > 65535 x %lld (use odf_score)", (long long)td);
     const int sp = lat_splits(m, n_docs, splits);
     size_t off[4];
     lat_layout(m, n_docs, sp, off);
@@ -1266,12 +1266,12 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0)
         return fail(ODF_E_INVALID_ARG, "workspace not 256-byte aligned");
     // code columns + 2 (else 1) tree-chunk buffers + reduction buffer + mbarriers
-    const size_t fixed = align_up(static_cast<uint64_t>(m->n_cols) * kTile, 1024) + kRedBytes + 64;
+    const size_t fixed = align_up(static_cast<uint64_t>(m->n_cols) * td, 1024) + kRedBytes + 64;
     const int nbuf = fixed + 2 * align_up(m->chunk_bytes, 1024) <= static_cast<size_t>(m->max_smem) ? 2 : 1;
     const size_t smem_apply = fixed + nbuf * align_up(m->chunk_bytes, 1024);
     KParams p = base_params(m, m->fused);
     p.n_docs = n_docs;
-    p.n_tiles = (n_docs + kTile - 1) / kTile;
+    p.n_tiles = (n_docs + td - 1) / td;
     p.scores = d_scores;
     p.stages = nbuf;
     uint8_t *ws = static_cast<uint8_t *>(d_workspace);
@@ -1285,7 +1285,7 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
         if (st != ODF_OK) return st;
         tmp = &tm;
     }
-    const size_t smem_bin = kFSubBytes + kMetaBytes + align_up(m->bord_stride, 16) + 64;
+    const size_t smem_bin = static_cast<size_t>(td) * kFSub * 4 + kMetaBytes + align_up(m->bord_stride, 16) + 64;
     if (smem_apply > static_cast<size_t>(m->max_smem))
         return fail(ODF_E_UNSUPPORTED, "latency path: %zu B of shared memory > %d", smem_apply, m->max_smem);
     int prev = 0;

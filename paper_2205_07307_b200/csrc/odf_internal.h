@@ -135,6 +135,7 @@ const void *kptr_mixed(int mode);      // mixed-height integer models, fused / a
 const void *kptr_t64_f(int mode, int depth);
 const void *kptr_t64_u(int mode, int depth);
 const void *kptr_t64_index(int depth);
+const void *kptr_t64_lat(int depth);  // K4 with 64-document tiles: apply (depth), binarize (-1)
 const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
 const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);
@@ -144,7 +145,7 @@ cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
                          cudaStream_t s);
 cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,
-                           size_t smem_bin, size_t smem_apply, cudaStream_t s);
+                           size_t smem_bin, size_t smem_apply, cudaStream_t s);  // p.tile_docs picks DPL
 cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cudaStream_t s);
 // Opt every kernel in to `smem` bytes of dynamic shared memory.
 cudaError_t prepare_kernels(int max_smem);

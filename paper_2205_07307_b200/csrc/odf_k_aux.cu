@@ -75,8 +75,13 @@ static const void *lat_fn()
 {
     return reinterpret_cast<const void *>(&odf_lat_apply_kernel<DEPTH>);
 }
-static const void *lat_apply_kernel(int depth)
+static const void *lat_binarize_kernel(int tile_docs)
 {
+    return tile_docs == 64 ? kptr_t64_lat(-1) : reinterpret_cast<const void *>(&odf_lat_binarize_kernel<4>);
+}
+static const void *lat_apply_kernel(int depth, int tile_docs = 128)
+{
+    if (tile_docs == 64) return kptr_t64_lat(depth);
     static const void *t[11] = {lat_fn<0>(), lat_fn<1>(), lat_fn<2>(), lat_fn<3>(),
                                 lat_fn<4>(), lat_fn<5>(), lat_fn<6>(), lat_fn<7>(),
                                 lat_fn<8>(), lat_fn<9>(), lat_fn<10>()};
@@ -95,7 +100,7 @@ cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap,
     cudaError_t e = cudaSuccess;
     if (p.n_fchunks > 0) {
         void *args[] = {&pc, &tm};
-        e = cudaLaunchKernel(reinterpret_cast<const void *>(&odf_lat_binarize_kernel),
+        e = cudaLaunchKernel(lat_binarize_kernel(p.tile_docs),
                              dim3(p.n_fchunks, static_cast<unsigned>(p.n_tiles)), dim3(kConsumerThreads),
                              args, smem_bin, s);
         if (e != cudaSuccess) return e;
@@ -116,7 +121,7 @@ cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void *args2[] = {&pc};
-    return cudaLaunchKernelExC(&cfg, lat_apply_kernel(depth), args2);
+    return cudaLaunchKernelExC(&cfg, lat_apply_kernel(depth, p.tile_docs), args2);
 }
 
 static cudaError_t opt_in(const void *f, int max_smem)
@@ -137,7 +142,8 @@ cudaError_t prepare_kernels(int max_smem)
                             main_kernel(MODE_FUSED, d, false, false, 2), main_kernel(MODE_APPLY, d, false, false, 2),
                             main_kernel(MODE_FUSED, d, false, false, 1, 64), main_kernel(MODE_APPLY, d, false, false, 1, 64),
                             main_kernel(MODE_FUSED, d, true, false, 1, 64), main_kernel(MODE_APPLY, d, true, false, 1, 64),
-                            index_kernel(d), index_kernel(d, 64), lat_apply_kernel(d)};
+                            index_kernel(d), index_kernel(d, 64), lat_apply_kernel(d),
+                            lat_apply_kernel(d, 64)};
         for (const void *f : fs) {
             cudaError_t e = opt_in(f, max_smem);
             if (e != cudaSuccess) return e;
@@ -152,7 +158,9 @@ cudaError_t prepare_kernels(int max_smem)
         cudaError_t e = opt_in(main_kernel(MODE_BINARIZE, 0, false, false, 1, 64), max_smem);
         if (e != cudaSuccess) return e;
     }
-    cudaError_t e = opt_in(reinterpret_cast<const void *>(&odf_lat_binarize_kernel), max_smem);
+    cudaError_t e = opt_in(lat_binarize_kernel(128), max_smem);
+    if (e != cudaSuccess) return e;
+    e = opt_in(lat_binarize_kernel(64), max_smem);
     if (e != cudaSuccess) return e;
     e = opt_in(main_kernel(MODE_BINARIZE, 0, false, true), max_smem);
     if (e != cudaSuccess) return e;

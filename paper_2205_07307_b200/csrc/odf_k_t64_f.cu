@@ -39,4 +39,18 @@ const void *kptr_t64_index(int depth)
     return (depth < 0 || depth > 10) ? nullptr : t[depth];
 }
 
+// K4 latency path for 64-document-tile models: binarize (kernel 1) and apply (kernel 2)
+template <int DEPTH>
+static const void *la()
+{
+    return reinterpret_cast<const void *>(&odf_lat_apply_kernel<DEPTH, 2>);
+}
+const void *kptr_t64_lat(int depth)  // depth -1: the binarize kernel
+{
+    static const void *t[11] = {la<0>(), la<1>(), la<2>(), la<3>(), la<4>(), la<5>(),
+                                la<6>(), la<7>(), la<8>(), la<9>(), la<10>()};
+    if (depth == -1) return reinterpret_cast<const void *>(&odf_lat_binarize_kernel<2>);
+    return (depth < 0 || depth > 10) ? nullptr : t[depth];
+}
+
 }  // namespace odf

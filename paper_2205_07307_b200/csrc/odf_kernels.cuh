@@ -1348,25 +1348,29 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // The association differs from the main path (tree ranges per split), so these
 // scores are held to the tolerance, not bit-exactness.
 // ---------------------------------------------------------------------------
-#ifdef ODF_KERNELS_AUX  // non-template kernels: defined in odf_k_aux.cu only
+// DPL: documents per lane of the model's tiles (4: 128-document tiles; 2: 64-document
+// tiles of wide-column models, whose column offsets are halved, CSH = 1)
+template <int DPL>
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_lat_binarize_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
+    constexpr int kT = 32 * DPL, NDL = DPL / 2, CSH = DPL == 4 ? 0 : 1;
+    constexpr uint32_t kBox = kT * kFSub * 4u;  // one TMA box: kT docs x 32 factors
     if (smem_addr(smem_raw) & 1023u) __trap();
     const int c = blockIdx.x;
     const int64_t tile = blockIdx.y;
-    const uint32_t t_off = 0, m_off = kFSubBytes, b_off = kFSubBytes + kMetaBytes;
+    const uint32_t t_off = 0, m_off = kBox, b_off = kBox + kMetaBytes;
     const uint32_t bar = b_off + ((p.bord_stride + 15u) & ~15u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
         const uint2 bc = p.bchunk[c];
-        mbar_expect_tx(bar, kFSubBytes + kMetaBytes + bc.y);
+        mbar_expect_tx(bar, kBox + kMetaBytes + bc.y);
         if (p.fm)
-            tma_load_2d(t_off, &tmap, static_cast<int>(tile * kTile), c * kFSub, bar);
+            tma_load_2d(t_off, &tmap, static_cast<int>(tile * kT), c * kFSub, bar);
         else
-            tma_load_2d(t_off, &tmap, c * kFSub, static_cast<int>(tile * kTile), bar);
+            tma_load_2d(t_off, &tmap, c * kFSub, static_cast<int>(tile * kT), bar);
         bulk_g2s(m_off, p.fmeta + c * kFSub, kMetaBytes, bar);
         if (bc.y) bulk_g2s(b_off, reinterpret_cast<const char *>(p.borders) + bc.x, bc.y, bar);
         if (c == 0) p.lat_counter[tile] = 0u;  // ticket for kernel (2), stream-ordered
@@ -1377,17 +1381,20 @@ __global__ void __launch_bounds__(kConsumerThreads)
     __syncthreads();
     mbar_wait(bar, 0);
     const GmemSink sink{p.lat_codes + tile * p.code_stride};
+    constexpr bool WIDE = DPL == 4;  // > 254-border factors: 128-document models only
     if (p.fm)
-        binarize_sub<2, true, true, true>(t_off, m_off, b_off, sink, warp >> 1, (warp & 1) << 6, lane);
+        binarize_sub<NDL, true, WIDE, true, GmemSink, CSH>(t_off, m_off, b_off, sink, warp >> 1,
+                                                           (warp & 1) * 32 * NDL, lane);
     else
-        binarize_sub<2, true, true, false>(t_off, m_off, b_off, sink, warp >> 1, (warp & 1) << 6, lane);
+        binarize_sub<NDL, true, WIDE, false, GmemSink, CSH>(t_off, m_off, b_off, sink, warp >> 1,
+                                                            (warp & 1) * 32 * NDL, lane);
 }
-#endif
 
-template <int DEPTH>
+template <int DEPTH, int DPL = 4>
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_lat_apply_kernel(const KParams p)
 {
+    constexpr int kT = 32 * DPL;  // documents per tile
     if (smem_addr(smem_raw) & 1023u) __trap();
     const int split = blockIdx.x, S = gridDim.x;
     const int64_t tile = blockIdx.y;
@@ -1396,7 +1403,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     // reduction buffer, mbarriers [codes, chunk buffer 0, chunk buffer 1]; everything is
     // staged with bulk copies (cp.async.bulk), not thread loops
     const uint32_t bins = 0;
-    const uint32_t cols_bytes = static_cast<uint32_t>(p.n_cols) * kTile;
+    const uint32_t cols_bytes = static_cast<uint32_t>(p.n_cols) * kT;
     const uint32_t chunk_al = (p.chunk_bytes + 1023u) & ~1023u;
     const uint32_t chunk0 = (cols_bytes + 1023u) & ~1023u;
     const int nbuf = p.stages;
@@ -1425,39 +1432,39 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     __syncthreads();  // barrier initialisation visible to every thread
     if (cols_bytes > 0) mbar_wait(bar, 0);
-    Acc<false> acc;
-    const Lane ln = make_lane(p, sabs(bins) + lane * 4u);  // absolute (tree_level)
+    Acc<false, DPL> acc;
+    const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_level)
     uint32_t ph0 = 0, ph1 = 0;
     for (int c = c_lo, i = 0; c < c_hi; ++c, ++i) {
         const int b = nbuf == 2 ? (i & 1) : 0;
         mbar_wait(bar + 8u + 8u * b, b ? ph1 : ph0);
         if (b) ph1 ^= 1u; else ph0 ^= 1u;
-        apply_chunk<DEPTH, false>(chunk0 + b * chunk_al, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
+        apply_chunk<DEPTH, false, DPL>(chunk0 + b * chunk_al, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
         if (c + nbuf < c_hi) {  // refill buffer b once every warp's gathers from it are done
             acc.pin(bar + 24u);
             __syncthreads();
             if (tid == 0) stage_chunk(c + nbuf, b);
         }
     }
-    acc.to_red(red, warp, lane * 4, kTile);
+    acc.to_red(red, warp, lane * DPL, kT);
     __syncthreads();
-    float *part = p.lat_partial + (tile * S) * kTile;
-    if (tid < kTile) {
+    float *part = p.lat_partial + (tile * S) * kT;
+    if (tid < kT) {
         float v = lds_f32(red + tid * 4);
 #pragma unroll
-        for (int w = 1; w < kConsumerWarps; ++w) v += lds_f32(red + w * (kTile * 4) + tid * 4);
-        part[split * kTile + tid] = v;
+        for (int w = 1; w < kConsumerWarps; ++w) v += lds_f32(red + w * (kT * 4) + tid * 4);
+        part[split * kT + tid] = v;
     }
     __threadfence();
     __syncthreads();
     __shared__ uint32_t last;
     if (tid == 0) last = (atomicAdd(p.lat_counter + tile, 1u) == static_cast<uint32_t>(S - 1)) ? 1u : 0u;
     __syncthreads();
-    if (last && tid < kTile) {
+    if (last && tid < kT) {
         __threadfence();
         float v = __ldcg(part + tid);
-        for (int s2 = 1; s2 < S; ++s2) v += __ldcg(part + s2 * kTile + tid);
-        const int64_t doc = tile * kTile + tid;
+        for (int s2 = 1; s2 < S; ++s2) v += __ldcg(part + s2 * kT + tid);
+        const int64_t doc = tile * kT + tid;
         if (doc < p.n_docs) p.scores[doc] = v;
     }
 }

@@ -591,9 +591,6 @@ def test_wide_column_model_integer_and_latency_path():
         cuda_model(deep)
     assert e.value.status == 2 and "64 documents" in str(e.value)
     m = cuda_model(case)
-    with pytest.raises(OdfError) as e:  # the latency path keeps 128-document tiles
-        m.score_latency(x, m.latency_workspace(500))
-    assert e.value.status == 2
     s = m.score(x, tile_docs=0)
     s64 = m.score(x, tile_docs=64)
     assert torch.equal(s.view(torch.int32), s64.view(torch.int32))
@@ -602,6 +599,37 @@ def test_wide_column_model_integer_and_latency_path():
             m.score(x, tile_docs=td)
         assert e.value.status == st
     torch.cuda.synchronize()
+    m.close()
+
+
+@pytest.mark.parametrize("n_docs", [1, 63, 64, 65, 129, 500])
+@pytest.mark.parametrize("splits", [0, 1, 3])
+def test_wide_column_latency_path(n_docs, splits):
+    """K4 on a 64-document-tile model (1,950 factors, P:168's width): within the
+    tolerance of the oracle and of odf_score, deterministic, graph-capturable."""
+    import torch
+    case = _wide_columns_case(n_docs, n_trees=400)
+    m = cuda_model(case)
+    assert m.info["bins_tile_docs"] == 64
+    x = to_dev(case.x)
+    ws = m.latency_workspace(n_docs, splits)
+    a = m.score_latency(x, ws, splits=splits).cpu().numpy()
+    b = m.score_latency(x, ws, splits=splits).cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    tol = tolerance(case.leaf_values, case.depth)
+    s64, _ = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, case.depth)
+    assert np.abs(a.astype(np.float64) - s64).max() <= tol
+    assert np.abs(a - m.score(x).cpu().numpy()).max() <= tol
+    out = torch.empty(n_docs, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    m.score_latency(x, ws, out=out, splits=splits)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        m.score_latency(x, ws, out=out, splits=splits)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), a.view(np.uint32))
     m.close()
 
 

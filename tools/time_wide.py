@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Timing of a P:168-width model (1,950 factors -> 64-document tiles) on 1 M documents:
-fused odf_score, binarize, apply (CUDA-event medians).  Prints one JSON line."""
+fused odf_score, binarize, apply (CUDA-event medians); and the K4 latency path on
+batches of 100 / 1000 / 5000 of those documents (per-call CUDA-event medians: direct
+two-launch calls, and a captured graph replayed on a resident buffer).  One JSON line."""
 import json
 import os
 import sys
@@ -32,6 +34,21 @@ def main():
            "binarize_ms": timeit(lambda: m.binarize(x, out=bins), 10),
            "apply_ms": timeit(lambda: m.apply(bins, n, out=out), 10)}
     res["fused_docs_per_s"] = n / (res["fused_ms"] / 1e3)
+    lat = {}
+    for B in (100, 1000, 5000):
+        xb = x[:B].contiguous()
+        ws = m.latency_workspace(B)
+        ob = torch.empty(B, device="cuda")
+        e = {"direct_us": timeit(lambda: m.score_latency(xb, ws, out=ob), 200) * 1e3,
+             "fused_us": timeit(lambda: m.score(xb, out=ob), 200) * 1e3}
+        g = torch.cuda.CUDAGraph()
+        m.score_latency(xb, ws, out=ob)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            m.score_latency(xb, ws, out=ob)
+        e["graph_us"] = timeit(g.replay, 200) * 1e3
+        lat[str(B)] = e
+    res["latency_p50"] = lat
     print(json.dumps(res), flush=True)
 
 
