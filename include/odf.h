@@ -281,14 +281,22 @@ ODF_API odf_status odf_index_fingerprint(const odf_model *m, const uint8_t *d_bi
  * odf_latency_workspace_bytes(m, n_docs, splits) bytes (same `splits`), owned by
  * the caller; concurrent calls need distinct workspaces.  Same argument rules as
  * odf_score, and n_docs <= 65535 x bins_tile_docs (ODF_E_INVALID_ARG above: tiles
- * are a grid dimension; this is the small-batch path).  fp32-leaf models only
- * (ODF_E_UNSUPPORTED for u32 leaves).  Capturable in a CUDA graph (two
+ * are a grid dimension; this is the small-batch path).  fp32-leaf models (integer
+ * models: odf_score_latency_u64, ODF_E_INVALID_ARG here).  Capturable in a CUDA graph (two
  * kernel nodes; the factor pointer is baked into the captured tensor map, so a
  * graph serves one input buffer, tests/test_gpu_parity.py::test_latency_graph). */
 ODF_API size_t odf_latency_workspace_bytes(const odf_model *m, int64_t n_docs, int32_t splits);
 ODF_API odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t n_docs,
                                      int64_t ld, float *d_scores, int32_t splits,
                                      void *d_workspace, size_t workspace_bytes, void *stream);
+/* The latency path for integer-leaf models (NEXT-1; mixed heights, NEXT-2, included):
+ * outputs as odf_score_u64 (either may be NULL, not both).  The per-split partial
+ * sums are u64 and added exactly, so the results equal odf_score_u64's bit for bit.
+ * Workspace: odf_latency_workspace_bytes of this model (8-byte partials).  fp32
+ * models: ODF_E_INVALID_ARG.  Otherwise as odf_score_latency.                  */
+ODF_API odf_status odf_score_latency_u64(const odf_model *m, const float *d_factors, int64_t n_docs,
+                                         int64_t ld, uint64_t *d_sums, double *d_scores, int32_t splits,
+                                         void *d_workspace, size_t workspace_bytes, void *stream);
 
 /* End-to-end from HOST memory: h_factors [n_docs x ld] fp32 (pinned or not;
  * pinned is faster) -> h_scores [n_docs].  Copies host->device, runs the fused

@@ -1232,7 +1232,7 @@ static void lat_layout(const odf_model *m, int64_t n_docs, int sp, size_t off[4]
     auto a256 = [](size_t v) { return (v + 255) / 256 * 256; };
     off[0] = 0;
     off[1] = a256(static_cast<size_t>(tiles) * (m->n_cols + 1) * td);
-    off[2] = off[1] + a256(static_cast<size_t>(tiles) * sp * td * 4);
+    off[2] = off[1] + a256(static_cast<size_t>(tiles) * sp * td * (m->leaf_u32 ? 8 : 4));  // partials
     off[3] = off[2] + a256(static_cast<size_t>(tiles) * 4);
 }
 
@@ -1244,16 +1244,13 @@ size_t odf_latency_workspace_bytes(const odf_model *m, int64_t n_docs, int32_t s
     return off[3];
 }
 
-odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
-                             float *d_scores, int32_t splits, void *d_workspace,
-                             size_t workspace_bytes, void *stream)
+static odf_status run_latency(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                              float *d_scores, uint64_t *d_sums, double *d_dscores, int32_t splits,
+                              void *d_workspace, size_t workspace_bytes, void *stream)
 {
-    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
-    if (m->leaf_u32) return fail(ODF_E_UNSUPPORTED, "latency path: fp32-leaf models only");
     odf_status st = check_factors(m, d_factors, n_docs, ld);
     if (st != ODF_OK) return st;
     if (n_docs == 0) return ok();
-    if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
     const int64_t td = m->tile_docs;  // 128, or 64 for wide-column models
     if ((n_docs + td - 1) / td > 65535)  // tiles are the grid's y dimension
         return fail(ODF_E_INVALID_ARG, "latency path: n_docs > 65535 x %lld (use odf_score)", (long long)td);
@@ -1266,13 +1263,16 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0)
         return fail(ODF_E_INVALID_ARG, "workspace not 256-byte aligned");
     // code columns + 2 (else 1) tree-chunk buffers + reduction buffer + mbarriers
-    const size_t fixed = align_up(static_cast<uint64_t>(m->n_cols) * td, 1024) + kRedBytes + 64;
+    const size_t fixed = align_up(static_cast<uint64_t>(m->n_cols) * td, 1024) +
+                         (m->leaf_u32 ? 2 : 1) * kRedBytes + 64;
     const int nbuf = fixed + 2 * align_up(m->chunk_bytes, 1024) <= static_cast<size_t>(m->max_smem) ? 2 : 1;
     const size_t smem_apply = fixed + nbuf * align_up(m->chunk_bytes, 1024);
     KParams p = base_params(m, m->fused);
     p.n_docs = n_docs;
     p.n_tiles = (n_docs + td - 1) / td;
     p.scores = d_scores;
+    p.sums = reinterpret_cast<unsigned long long *>(d_sums);
+    p.dscores = d_dscores;
     p.stages = nbuf;
     uint8_t *ws = static_cast<uint8_t *>(d_workspace);
     p.lat_codes = ws + off[0];
@@ -1291,11 +1291,34 @@ odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != m->device) cudaSetDevice(m->device);
-    cudaError_t e = launch_latency(m->depth, p, tmp, sp, smem_bin, smem_apply,
+    cudaError_t e = launch_latency(m->kdepth, p, tmp, sp, smem_bin, smem_apply,
                                    static_cast<cudaStream_t>(stream));
     if (prev != m->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "latency kernels");
     return ok();
+}
+
+odf_status odf_score_latency(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                             float *d_scores, int32_t splits, void *d_workspace,
+                             size_t workspace_bytes, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (m->leaf_u32) return fail(ODF_E_INVALID_ARG, "integer-leaf model: use odf_score_latency_u64");
+    if (n_docs > 0 && !d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    return run_latency(m, d_factors, n_docs, ld, d_scores, nullptr, nullptr, splits, d_workspace,
+                       workspace_bytes, stream);
+}
+
+odf_status odf_score_latency_u64(const odf_model *m, const float *d_factors, int64_t n_docs, int64_t ld,
+                                 uint64_t *d_sums, double *d_scores, int32_t splits, void *d_workspace,
+                                 size_t workspace_bytes, void *stream)
+{
+    if (!m) return fail(ODF_E_INVALID_ARG, "model is NULL");
+    if (!m->leaf_u32) return fail(ODF_E_INVALID_ARG, "fp32-leaf model: use odf_score_latency");
+    if (n_docs > 0 && !d_sums && !d_scores)
+        return fail(ODF_E_INVALID_ARG, "d_sums and d_scores are both NULL");
+    return run_latency(m, d_factors, n_docs, ld, nullptr, d_sums, d_scores, splits, d_workspace,
+                       workspace_bytes, stream);
 }
 
 static odf_status score_host_impl(odf_model *m, const float *h_factors, int64_t n_docs, int64_t ld,

@@ -136,6 +136,7 @@ const void *kptr_t64_f(int mode, int depth);
 const void *kptr_t64_u(int mode, int depth);
 const void *kptr_t64_index(int depth);
 const void *kptr_t64_lat(int depth);  // K4 with 64-document tiles: apply (depth), binarize (-1)
+const void *kptr_lat_u(int depth, int tile_docs);  // K4 apply, u32 leaves: depth 0..10 or kMixedDepth
 const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
 const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);

@@ -79,8 +79,9 @@ static const void *lat_binarize_kernel(int tile_docs)
 {
     return tile_docs == 64 ? kptr_t64_lat(-1) : reinterpret_cast<const void *>(&odf_lat_binarize_kernel<4>);
 }
-static const void *lat_apply_kernel(int depth, int tile_docs = 128)
+static const void *lat_apply_kernel(int depth, int tile_docs = 128, bool u32 = false)
 {
+    if (u32) return kptr_lat_u(depth, tile_docs);
     if (tile_docs == 64) return kptr_t64_lat(depth);
     static const void *t[11] = {lat_fn<0>(), lat_fn<1>(), lat_fn<2>(), lat_fn<3>(),
                                 lat_fn<4>(), lat_fn<5>(), lat_fn<6>(), lat_fn<7>(),
@@ -121,7 +122,9 @@ cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void *args2[] = {&pc};
-    return cudaLaunchKernelExC(&cfg, lat_apply_kernel(depth, p.tile_docs), args2);
+    const void *f = lat_apply_kernel(depth, p.tile_docs, p.leaf_u32 != 0);
+    if (!f) return cudaErrorInvalidValue;
+    return cudaLaunchKernelExC(&cfg, f, args2);
 }
 
 static cudaError_t opt_in(const void *f, int max_smem)
@@ -149,6 +152,11 @@ cudaError_t prepare_kernels(int max_smem)
             if (e != cudaSuccess) return e;
         }
     }
+    for (int d = 0; d <= kMixedDepth; ++d)
+        for (int td : {128, 64}) {
+            cudaError_t e = opt_in(lat_apply_kernel(d, td, true), max_smem);
+            if (e != cudaSuccess) return e;
+        }
     for (int mode : {MODE_FUSED, MODE_APPLY})
         for (int td : {128, 64}) {
             cudaError_t e = opt_in(main_kernel(mode, kMixedDepth, true, false, 1, td), max_smem);

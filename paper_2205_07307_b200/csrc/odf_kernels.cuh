@@ -26,6 +26,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <type_traits>
+
 #pragma once
 #include "odf_internal.h"
 
@@ -1390,11 +1392,16 @@ __global__ void __launch_bounds__(kConsumerThreads)
                                                             (warp & 1) * 32 * NDL, lane);
 }
 
-template <int DEPTH, int DPL = 4>
+// U32: integer leaves (NEXT-1), u64 partials per split summed exactly (order-free: the
+// result equals odf_score_u64 bit for bit); DEPTH == kMixedDepth: height segments
+// (NEXT-2), each chunk applied at its segment's depth.
+template <int DEPTH, int DPL = 4, bool U32 = false>
 __global__ void __launch_bounds__(kConsumerThreads)
     odf_lat_apply_kernel(const KParams p)
 {
     constexpr int kT = 32 * DPL;  // documents per tile
+    constexpr bool MIXED = DEPTH == kMixedDepth;
+    static_assert(!MIXED || U32, "mixed-height models: integer answers");
     if (smem_addr(smem_raw) & 1023u) __trap();
     const int split = blockIdx.x, S = gridDim.x;
     const int64_t tile = blockIdx.y;
@@ -1408,13 +1415,26 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const uint32_t chunk0 = (cols_bytes + 1023u) & ~1023u;
     const int nbuf = p.stages;
     const uint32_t red = chunk0 + nbuf * chunk_al;
-    const uint32_t bar = red + kRedBytes;
+    const uint32_t bar = red + Acc<U32, DPL>::kRed;
     const int c_lo = static_cast<int>(static_cast<int64_t>(split) * p.n_tchunks / S);
     const int c_hi = static_cast<int>(static_cast<int64_t>(split + 1) * p.n_tchunks / S);
+    // chunk c of the stream: its segment (mixed-height models; one segment otherwise)
+    auto seg_of = [&](int c) {
+        int sg = 0;
+        if constexpr (MIXED)
+            while (sg + 1 < p.n_seg && c >= p.seg[sg].n_chunks) c -= p.seg[sg++].n_chunks;
+        return make_int2(sg, c);
+    };
     auto stage_chunk = [&](int c, int b) {  // one thread
-        mbar_expect_tx(bar + 8u + 8u * b, p.chunk_bytes);
-        bulk_g2s(chunk0 + b * chunk_al, p.chunks + static_cast<size_t>(c) * p.chunk_bytes, p.chunk_bytes,
-                 bar + 8u + 8u * b);
+        uint32_t cb = p.chunk_bytes;
+        const uint8_t *src = p.chunks + static_cast<size_t>(c) * p.chunk_bytes;
+        if constexpr (MIXED) {
+            const int2 sc = seg_of(c);
+            cb = p.seg[sc.x].chunk_bytes;
+            src = p.chunks + p.seg[sc.x].byte_off + static_cast<size_t>(sc.y) * cb;
+        }
+        mbar_expect_tx(bar + 8u + 8u * b, cb);
+        bulk_g2s(chunk0 + b * chunk_al, src, cb, bar + 8u + 8u * b);
     };
     if (tid == 0) {
         mbar_init(bar, 1);
@@ -1432,14 +1452,33 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     __syncthreads();  // barrier initialisation visible to every thread
     if (cols_bytes > 0) mbar_wait(bar, 0);
-    Acc<false, DPL> acc;
+    Acc<U32, DPL> acc;
     const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_level)
     uint32_t ph0 = 0, ph1 = 0;
     for (int c = c_lo, i = 0; c < c_hi; ++c, ++i) {
         const int b = nbuf == 2 ? (i & 1) : 0;
         mbar_wait(bar + 8u + 8u * b, b ? ph1 : ph0);
         if (b) ph1 ^= 1u; else ph0 ^= 1u;
-        apply_chunk<DEPTH, false, DPL>(chunk0 + b * chunk_al, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
+        const uint32_t cb = chunk0 + b * chunk_al;
+        if constexpr (MIXED) {
+            const SegP &g = p.seg[seg_of(c).x];
+            const int nk = g.tc / kConsumerWarps;
+            switch (g.depth) {  // warp-uniform: one branch per chunk
+                case 0: apply_chunk<0, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 1: apply_chunk<1, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 2: apply_chunk<2, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 3: apply_chunk<3, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 4: apply_chunk<4, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 5: apply_chunk<5, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 6: apply_chunk<6, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 7: apply_chunk<7, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 8: apply_chunk<8, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                case 9: apply_chunk<9, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+                default: apply_chunk<10, true, DPL>(cb, g.desc_bytes, ln, warp, nk, acc); break;
+            }
+        } else {
+            apply_chunk<DEPTH, U32, DPL>(cb, p.desc_bytes, ln, warp, p.tc / kConsumerWarps, acc);
+        }
         if (c + nbuf < c_hi) {  // refill buffer b once every warp's gathers from it are done
             acc.pin(bar + 24u);
             __syncthreads();
@@ -1448,11 +1487,12 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     acc.to_red(red, warp, lane * DPL, kT);
     __syncthreads();
-    float *part = p.lat_partial + (tile * S) * kT;
+    using Part = typename std::conditional<U32, unsigned long long, float>::type;
+    Part *part = reinterpret_cast<Part *>(p.lat_partial) + (tile * S) * kT;
     if (tid < kT) {
-        float v = lds_f32(red + tid * 4);
+        Part v = sld<Part>(red + tid * sizeof(Part));
 #pragma unroll
-        for (int w = 1; w < kConsumerWarps; ++w) v += lds_f32(red + w * (kT * 4) + tid * 4);
+        for (int w = 1; w < kConsumerWarps; ++w) v += sld<Part>(red + (w * kT + tid) * sizeof(Part));
         part[split * kT + tid] = v;
     }
     __threadfence();
@@ -1462,10 +1502,20 @@ __global__ void __launch_bounds__(kConsumerThreads)
     __syncthreads();
     if (last && tid < kT) {
         __threadfence();
-        float v = __ldcg(part + tid);
+        Part v = __ldcg(part + tid);
         for (int s2 = 1; s2 < S; ++s2) v += __ldcg(part + s2 * kT + tid);
         const int64_t doc = tile * kT + tid;
-        if (doc < p.n_docs) p.scores[doc] = v;
+        if (doc < p.n_docs) {
+            if constexpr (U32) {
+                if (p.sums) p.sums[doc] = v;
+                // (R - 2^31) * S + B, rounded op by op (no FMA contraction)
+                if (p.dscores)
+                    p.dscores[doc] = __dadd_rn(
+                        __dmul_rn(__dsub_rn(static_cast<double>(v), 2147483648.0), p.scale), p.bias);
+            } else {
+                p.scores[doc] = v;
+            }
+        }
     }
 }
 

@@ -147,6 +147,8 @@ def lib():
     L.odf_score_latency.restype = ctypes.c_int
     L.odf_score_latency.argtypes = [_vp, _vp, _i64, _i64, _vp, _i32, _vp, ctypes.c_size_t, _vp]
     L.odf_score_host.restype = ctypes.c_int
+    L.odf_score_latency_u64.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp, _i32, _vp, ctypes.c_size_t, _vp]
+    L.odf_score_latency_u64.restype = ctypes.c_int
     L.odf_score_host.argtypes = [_vp, _vp, _i64, _i64, _vp, _i64, _vp]
     _lib = L
     return L
@@ -158,7 +160,7 @@ ABI_SYMBOLS = ("odf_version", "odf_last_error", "odf_load_model", "odf_free_mode
                "odf_latency_workspace_bytes", "odf_score_latency", "odf_load_model_ex",
                "odf_score_u64", "odf_apply_u64", "odf_load_model_paper", "odf_binarize_fm",
                "odf_score_fm", "odf_bits_layout", "odf_bits_from_bins", "odf_apply_bits",
-               "odf_score_tiles", "odf_apply_tiles")
+               "odf_score_tiles", "odf_apply_tiles", "odf_score_latency_u64")
 
 
 def _check(status: int):
@@ -347,6 +349,19 @@ class Model:
                                        _ptr(workspace), workspace.numel(),
                                        _stream(stream, self._dev())))
         return out
+
+    def score_latency_u64(self, x: torch.Tensor, workspace: torch.Tensor, splits: int = 0, stream=None):
+        """K4 for integer-leaf models: (u64 sums R as int64 bits, (R - 2^31)*S + B), equal to
+        score_u64 bit for bit."""
+        n, ld = self._check_x(x)
+        if not (workspace.is_cuda and workspace.device == self._dev() and workspace.dtype == torch.uint8):
+            raise OdfError(1, f"workspace must be a uint8 tensor on {self._dev()}")
+        sums = torch.empty(n, dtype=torch.int64, device=self._dev())
+        sc = torch.empty(n, dtype=torch.float64, device=self._dev())
+        _check(lib().odf_score_latency_u64(self._h, _ptr(x), n, ld, _ptr(sums), _ptr(sc), int(splits),
+                                           _ptr(workspace), workspace.numel(),
+                                           _stream(stream, self._dev())))
+        return sums, sc
 
     def score_u64(self, x: torch.Tensor, stream=None):
         """Integer-leaf model: (u64 sums R as int64 bits, (R - 2^31)*S + B as float64)."""

@@ -523,9 +523,17 @@ def test_integer_leaves_exact(depth, n_docs, n_trees):
     assert np.array_equal(sums2.cpu().numpy().view(np.uint64), want)
     fin = oracle.finalize(want, S, B)
     assert np.array_equal(sc.cpu().numpy(), fin) and np.array_equal(sc2.cpu().numpy(), fin)
+    # the latency path (K4): u64 partials per split, exact -> bit-identical for any split
+    for splits in (0, 1, 3):
+        ws = m.latency_workspace(n_docs, splits)
+        s3, sc3 = m.score_latency_u64(x, ws, splits=splits)
+        assert np.array_equal(s3.cpu().numpy().view(np.uint64), want)
+        assert np.array_equal(sc3.cpu().numpy(), fin)
     from paper_2205_07307_b200 import OdfError
     with pytest.raises(OdfError):
         m.score(x)
+    with pytest.raises(OdfError):
+        m.score_latency(x, m.latency_workspace(n_docs))
     torch.cuda.synchronize()
     m.close()
 
@@ -583,6 +591,8 @@ def test_wide_column_model_integer_and_latency_path():
     want = oracle.score_u64(case.x, case.feature_index, case.thresholds, lv, 6)
     assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
     assert np.array_equal(sums2.cpu().numpy().view(np.uint64), want)
+    sums3, _ = m.score_latency_u64(x, m.latency_workspace(500))  # K4, 64-document tiles
+    assert np.array_equal(sums3.cpu().numpy().view(np.uint64), want)
     m.close()
     # depth 10 at this width: 16-tree chunks of 4 KB tables (66 KB) x 2 ring slots do not
     # fit next to even a 64-document code block -> ODF_E_UNSUPPORTED, naming the bound
@@ -668,6 +678,11 @@ def test_paper_native_import(stc, n_binary, n_features, pad_heights):
     # two-stage (binarize + apply_u64) gives the same exact sums
     s2, _ = m.apply_u64(m.binarize(xd), D)
     assert np.array_equal(s2.cpu().numpy().view(np.uint64), want)
+    # the latency path (K4, per-height segments of a mixed model included), exact
+    for splits in (0, 5):
+        s3, sc3 = m.score_latency_u64(xd, m.latency_workspace(D, splits), splits=splits)
+        assert np.array_equal(s3.cpu().numpy().view(np.uint64), want)
+        assert np.array_equal(sc3.cpu().numpy(), oracle.finalize(want, pm.scale, pm.bias))
     heights = [h for h in range(len(stc)) if stc[h] > 0]
     if not pad_heights and len(heights) > 1:  # mixed model: no per-tree index export
         from paper_2205_07307_b200 import OdfError

@@ -5,6 +5,8 @@ odf_score_u64 (fused, exact u64 sums) per height segment and in the padded
 uniform-depth form; CUDA-event medians.  Scaled: 1,000,000 documents x 1,000
 factors U(0,1), 80 binary features per factor (155,377 over 1,950), and
 10,000 trees: 9,990 of depth 6, 3 of depth 8, 1 of depth 7, 1 each of depths 0..5.
+Also the K4 latency path (odf_score_latency_u64) on batches of 100 / 1000 / 5000 of
+those documents against the fused launch (CUDA-event medians, sums checked equal).
 
     python tools/bench_mixed.py [--docs N] [--reps R]
 """
@@ -48,6 +50,17 @@ def main():
             sums[key] = m.score_u64(x)[0].cpu().numpy()
             res[key + "_ms"] = timeit(lambda: m.score_u64(x), a.reps)
             res[key + "_docs_per_s"] = a.docs / (res[key + "_ms"] / 1e3)
+            if not pad:  # the K4 latency path on small batches of the same model (exact u64)
+                lat = {}
+                for B in (100, 1000, 5000):
+                    xb = x[:B].contiguous()
+                    ws = m.latency_workspace(B)
+                    want = m.score_u64(xb)[0]
+                    got = m.score_latency_u64(xb, ws)[0]
+                    lat[str(B)] = {"k4_us": timeit(lambda: m.score_latency_u64(xb, ws), 200) * 1e3,
+                                   "fused_us": timeit(lambda: m.score_u64(xb), 200) * 1e3,
+                                   "identical": bool(torch.equal(got, want))}
+                res["latency_p50_per_height"] = lat
             m.close()
         # reference: the same 10,000 trees all at depth 6 (the cost floor of this mix)
         pm6 = synth.paper_model(168, F, 80 * F, [0] * 6 + [sum(stc)])
