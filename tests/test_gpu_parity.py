@@ -366,6 +366,29 @@ def test_tile_256_exact_leaves_and_many_tiles():
     m.close()
 
 
+@pytest.mark.parametrize("depth", list(range(0, 11)))
+def test_tile_256_every_depth_exact(depth):
+    """256-document tiles at every depth (each depth has its own tree-item size, ring
+    sub-slot count and factor-job span): exact-arithmetic leaves, fused and two-stage
+    bit-exact against the oracle's fp32 rounding and equal to 128-document tiles, over
+    many tiles per SM (the sub-slot ring wraps many times; ragged last tile)."""
+    import torch
+    n_docs = 148 * 256 * 3 + 77
+    case = synth.tiny_case(seed=700 + depth, n_docs=n_docs, n_features=40, n_trees=48 + 16 * depth,
+                           depth=depth, pool=24, exact_leaves=True)
+    m = cuda_model(case)
+    assert m.info["max_tile_docs"] == 256, m.info
+    x = to_dev(case.x)
+    bins = m.binarize(x)
+    outs = [m.score(x, tile_docs=256), m.apply(bins, n_docs, tile_docs=256),
+            m.score(x, tile_docs=128)]
+    torch.cuda.synchronize()
+    _, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, case.depth)
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), s32)
+    m.close()
+
+
 def test_tile_width_errors():
     from paper_2205_07307_b200 import OdfError
     case = synth.tiny_case(3, n_docs=300)
