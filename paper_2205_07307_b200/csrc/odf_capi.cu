@@ -783,7 +783,10 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
                 const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
                                             : static_cast<uint32_t>(colB_of[f]) + c - 1u;
                 const uint32_t K = k - 127u * c + 1u;
-                if (desc8(sdepth)) {
+                if (desc_fmt(sdepth) == DESC_SPLIT) {
+                    desc[l] = col * kTile;
+                    desc[sdepth + l / 4] |= (128u - K) << (8 * (l % 4));
+                } else if (desc_fmt(sdepth) == DESC8) {
                     desc[2 * l] = col * kTile;
                     desc[2 * l + 1] = (128u - K) * 0x01010101u;
                 } else {

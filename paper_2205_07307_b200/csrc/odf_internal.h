@@ -26,15 +26,33 @@ constexpr uint32_t kNoCol = 0xFFFFFFFFu;
 // Level descriptor (u32): bits 19-31 = code column (col * 128 = desc >> 12), bits 0-7 =
 // 128 - K; a tree's descriptors are padded to a multiple of 4 levels (LDS.128 groups).
 // Level descriptor formats:
-//  * 8 bytes {col * 128, (128 - K) * 0x01010101} for depth <= 8: no byte
-//    replication (PRMT) per level, which relieves the ALU pipe (c3 fused -2.6 %);
-//  * 4 bytes (col << 19) | (128 - K) for depth 9-10, where the 8-byte form's extra
-//    descriptor bytes per staged tree cost more than it saves (c4 +1.4 %).
+//  * split, depth <= 8: the levels' col * 128 words, then the levels' (128 - K)
+//    bytes packed four per word (level l in byte l % 4 of word depth + l / 4),
+//    padded to 16 bytes: depth 6 = 32 B = two LDS.128.  A warp-uniform LDS.128
+//    costs two shared-memory wavefronts, so descriptor bytes per tree are
+//    shared-memory time; replicating K costs one PRMT per level;
+//  * 8 bytes {col * 128, (128 - K) * 0x01010101} (A/B builds): no PRMT, 48 B per
+//    depth-6 tree;
+//  * 4 bytes (col << 19) | (128 - K) for depth 9-10: address and K from one word.
 constexpr int kMaxDescCol = 8191;
-__host__ __device__ constexpr bool desc8(int depth) { return depth <= 8; }
+#ifndef ODF_DESC_SPLIT_MAX_DEPTH
+#define ODF_DESC_SPLIT_MAX_DEPTH 8  // A/B builds only
+#endif
+#ifndef ODF_DESC8_MAX_DEPTH
+#define ODF_DESC8_MAX_DEPTH 8  // A/B builds only
+#endif
+enum DescFmt : int { DESC4 = 0, DESC8 = 1, DESC_SPLIT = 2 };
+__host__ __device__ constexpr int desc_fmt(int depth)
+{
+    return depth <= ODF_DESC_SPLIT_MAX_DEPTH ? DESC_SPLIT : depth <= ODF_DESC8_MAX_DEPTH ? DESC8 : DESC4;
+}
+// words of a split-format tree that carry data: depth column words + ceil(depth / 4) K words
+__host__ __device__ constexpr int desc_split_words(int depth) { return depth + (depth + 3) / 4; }
 __host__ __device__ constexpr int desc_stride(int depth)
 {
-    return desc8(depth) ? ((depth + 1) & ~1) * 8 : ((depth + 3) & ~3) * 4;
+    return desc_fmt(depth) == DESC_SPLIT ? ((desc_split_words(depth) + 3) & ~3) * 4
+           : desc_fmt(depth) == DESC8    ? ((depth + 1) & ~1) * 8
+                                         : ((depth + 3) & ~3) * 4;
 }
 __host__ __device__ constexpr int table_stride(int depth) { return depth <= 6 ? 256 : (4 << depth); }
 __host__ __device__ constexpr int trees_per_chunk(int depth)

@@ -598,63 +598,99 @@ __device__ __forceinline__ uint32_t code_word(uint32_t a)
     else return ldsa_u16(a);
 }
 
-template <int DEPTH, int DPL = 4>
-__device__ __forceinline__ void tree_level(uint32_t dsc, const Lane &ln, int l, uint32_t &lo,
-                                           uint32_t &hi)
+// One level's flags: the lane's code word of the level's column, and the byte-wise
+// "code >= K" flags in bit 7 of each byte (code + (128 - K) never carries out of its
+// byte); krep = (128 - K) in every byte.
+template <int DPL = 4>
+__device__ __forceinline__ uint32_t level_flags(uint32_t col128, uint32_t krep, const Lane &ln)
 {
-    // col * 128 (col * 64 for 64-document tiles); absolute address
-    const uint32_t w = code_word<DPL>(ln.bins + (dsc >> (DPL == 4 ? 12 : 13)));
-    const uint32_t s = (w + prmt(dsc, 0u, 0x0000u)) & 0x80808080u;
-    if (l < 8)
-        lo = (l == 0) ? s : ((lo >> 1) | s);
-    else
-        hi = (l == 8) ? s : ((hi >> 1) | s);
+    return (code_word<DPL>(ln.bins + (DPL == 4 ? col128 : col128 >> 1)) + krep) & 0x80808080u;
+}
+// OR_j f[j] >> (N-1-j) from independent pairs (f[j] >> 1 | f[j+1]), then merged
+// pair by pair: a shorter dependency chain than N serial shift-or steps (c3 fused
+// -0.9 %, c2 -2.7 %; the pairing measured better than a halving tree on c3 apply)
+template <int N>
+__device__ __forceinline__ uint32_t merge_flags(const uint32_t *f)
+{
+    if constexpr (N <= 0) {
+        return 0u;
+    } else if constexpr (N == 1) {
+        return f[0];
+    } else {
+        constexpr int H = N > 2 ? 2 : 1;
+        return (merge_flags<N - H>(f) >> H) | merge_flags<H>(f + (N - H));
+    }
 }
 
-// 8-byte descriptors (depth <= 8): {col * 128, (128 - K) replicated in every byte}
-template <int DEPTH, int DPL = 4>
-__device__ __forceinline__ void tree_level8(uint32_t col128, uint32_t krep, const Lane &ln, int l,
-                                            uint32_t &lo, uint32_t &hi)
+// Split-format descriptors of one tree, in registers (odf_internal.h): column
+// words, then K bytes; loaded as LDS.128 groups, the tail as LDS.64 / LDS.32.
+template <int DEPTH>
+struct SplitDesc {
+    static constexpr int NW = desc_split_words(DEPTH);
+    uint32_t w[NW > 0 ? (NW + 3) & ~3 : 1];
+};
+template <int DEPTH>
+__device__ __forceinline__ SplitDesc<DEPTH> load_split(uint32_t d)
 {
-    const uint32_t w = code_word<DPL>(ln.bins + (DPL == 4 ? col128 : col128 >> 1));
-    const uint32_t s = (w + krep) & 0x80808080u;
-    if (l < 8)
-        lo = (l == 0) ? s : ((lo >> 1) | s);
-    else
-        hi = (l == 8) ? s : ((hi >> 1) | s);
+    SplitDesc<DEPTH> s;
+    constexpr int NW = SplitDesc<DEPTH>::NW;
+#pragma unroll
+    for (int g = 0; g < NW; g += 4) {
+        if (g + 2 < NW) {
+            const uint4 q = lds_v4u(d + g * 4);
+            s.w[g] = q.x; s.w[g + 1] = q.y; s.w[g + 2] = q.z; s.w[g + 3] = q.w;
+        } else if (g + 1 < NW) {
+            const uint2 q = lds_v2u(d + g * 4);
+            s.w[g] = q.x; s.w[g + 1] = q.y;
+        } else {
+            s.w[g] = lds_u32(d + g * 4);
+        }
+    }
+    return s;
 }
 
+// The flags of every level of the tree whose descriptors start at d, merged into
+// lo (levels 0..7: after all levels, level l of a depth-D tree sits at bit
+// 8 - min(D,8) + l of each byte) and hi (levels 8..: level 8 + j at bit
+// 16 - D + j); the byte of lo (| hi's bits above) is the complemented index F.
 template <int DEPTH, int DPL = 4>
 __device__ __forceinline__ void tree_flags(uint32_t d, const Lane &ln, uint32_t &lo,
                                            uint32_t &hi)
 {
-    lo = 0;
-    hi = 0;
-    if constexpr (desc8(DEPTH)) {
+    uint32_t f[DEPTH > 0 ? DEPTH : 1];
+    if constexpr (desc_fmt(DEPTH) == DESC_SPLIT) {
+        const SplitDesc<DEPTH> sd = load_split<DEPTH>(d);
+#pragma unroll
+        for (int l = 0; l < DEPTH; ++l)
+            f[l] = level_flags<DPL>(sd.w[l], prmt(sd.w[DEPTH + l / 4], 0u, 0x1111u * (l & 3)), ln);
+    } else if constexpr (desc_fmt(DEPTH) == DESC8) {
 #pragma unroll
         for (int l = 0; l < DEPTH; l += 2) {  // one LDS.128 per two levels
             const uint4 q = lds_v4u(d + l * 8);
-            tree_level8<DEPTH, DPL>(q.x, q.y, ln, l, lo, hi);
-            if (l + 1 < DEPTH) tree_level8<DEPTH, DPL>(q.z, q.w, ln, l + 1, lo, hi);
+            f[l] = level_flags<DPL>(q.x, q.y, ln);
+            if (l + 1 < DEPTH) f[l + 1] = level_flags<DPL>(q.z, q.w, ln);
         }
     } else {
+        // 4-byte descriptors: col * 128 = dsc >> 12, the byte 128 - K replicated by PRMT
+        uint32_t w[DEPTH > 0 ? (DEPTH + 3) & ~3 : 1];
 #pragma unroll
-    for (int l = 0; l < DEPTH; l += 4) {
-        if (l + 2 < DEPTH) {  // 3 or 4 levels left: one LDS.128 (padding levels unused)
-            const uint4 q = lds_v4u(d + l * 4);
-            tree_level<DEPTH, DPL>(q.x, ln, l, lo, hi);
-            tree_level<DEPTH, DPL>(q.y, ln, l + 1, lo, hi);
-            tree_level<DEPTH, DPL>(q.z, ln, l + 2, lo, hi);
-            if (l + 3 < DEPTH) tree_level<DEPTH, DPL>(q.w, ln, l + 3, lo, hi);
-        } else if (l + 1 < DEPTH) {
-            const uint2 q = lds_v2u(d + l * 4);
-            tree_level<DEPTH, DPL>(q.x, ln, l, lo, hi);
-            tree_level<DEPTH, DPL>(q.y, ln, l + 1, lo, hi);
-        } else {
-            tree_level<DEPTH, DPL>(lds_u32(d + l * 4), ln, l, lo, hi);
+        for (int l = 0; l < DEPTH; l += 4) {
+            if (l + 2 < DEPTH) {  // 3 or 4 levels left: one LDS.128 (padding levels unused)
+                const uint4 q = lds_v4u(d + l * 4);
+                w[l] = q.x; w[l + 1] = q.y; w[l + 2] = q.z; w[l + 3] = q.w;
+            } else if (l + 1 < DEPTH) {
+                const uint2 q = lds_v2u(d + l * 4);
+                w[l] = q.x; w[l + 1] = q.y;
+            } else {
+                w[l] = lds_u32(d + l * 4);
+            }
         }
+#pragma unroll
+        for (int l = 0; l < DEPTH; ++l) f[l] = level_flags<DPL>(w[l] >> 12, prmt(w[l], 0u, 0x0000u), ln);
     }
-    }
+    constexpr int NLO = DEPTH < 8 ? DEPTH : 8;
+    lo = merge_flags<NLO>(f);
+    hi = merge_flags<DEPTH - NLO>(f + NLO);
 }
 
 // Complemented leaf index F of the lane's 4 documents.
@@ -699,11 +735,8 @@ __device__ __forceinline__ uint32_t swz_bank_hi(uint32_t lo, uint32_t h)
 // Absolute shared-window addresses of the 4 leaves (tables reversed and
 // bank-swizzled; tb = the table base, absolute and 256-aligned).
 template <int DEPTH, int DPL = 4>
-__device__ __forceinline__ void leaf_addrs(uint32_t d, const Lane &ln, uint32_t tb,
-                                           uint32_t a[DPL])
+__device__ __forceinline__ void addrs_from_flags(uint32_t lo, uint32_t hi, uint32_t tb, uint32_t a[DPL])
 {
-    uint32_t lo, hi;
-    tree_flags<DEPTH, DPL>(d, ln, lo, hi);
     if constexpr (DEPTH <= 6) {
         // byte = F << (8-DEPTH); want 4F in the low byte of a 256-aligned base
         if constexpr (DEPTH < 6 && DEPTH > 0) lo >>= (6 - DEPTH);
@@ -723,6 +756,14 @@ __device__ __forceinline__ void leaf_addrs(uint32_t d, const Lane &ln, uint32_t 
         for (int n = 0; n < DPL; ++n)
             a[n] = tb + (prmt(lo, h, 0xCC00u | ((4u + n) << 4) | n) << 2);
     }
+}
+template <int DEPTH, int DPL = 4>
+__device__ __forceinline__ void leaf_addrs(uint32_t d, const Lane &ln, uint32_t tb,
+                                           uint32_t a[DPL])
+{
+    uint32_t lo, hi;
+    tree_flags<DEPTH, DPL>(d, ln, lo, hi);
+    addrs_from_flags<DEPTH, DPL>(lo, hi, tb, a);
 }
 
 
@@ -828,8 +869,10 @@ template <int DEPTH, bool U32, int DPL = 4>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
                                             int warp, int nk, Acc<U32, DPL> &acc)
 {
-    // chunks hold nk * 16 trees (the last one padded with zero-answer trees); a
-    // multiple of 4 trees per warp runs 4 trees per iteration (warp-uniform choice)
+    // chunks hold nk * 16 trees (the last one padded with zero-answer trees).
+    // (A software pipeline loading the next pair's descriptors during this pair was
+    // slower: c3 fused 6.43 -> 7.66 ms.)
+    // a multiple of 4 trees per warp runs 4 trees per iteration (warp-uniform choice)
     if (DEPTH <= 6 && (nk & 3) == 0) {
 #pragma unroll 4
         for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
@@ -1118,7 +1161,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
     // ========================= consumer warps =========================
     const int tid = threadIdx.x;
     const int half = H == 1 ? 0 : warp / kSlots, tslot = H == 1 ? warp : warp % kSlots;
-    const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * DPL);  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * DPL);  // absolute (tree_flags)
     const uint32_t desc_off = H == 1 ? p.desc_bytes : p.hdesc_bytes;  // tables in a ring slot
     const int nk = H == 1 ? p.tc / kConsumerWarps : p.tc / (2 * kSlots);  // trees per job per warp
     uint32_t slot = 0, ph = 0, bph = 0;
@@ -1287,7 +1330,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             expand_splits<DPL>(p, bins, tid, kConsumerThreads);
         __syncthreads();
     }
-    const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_flags)
     const int64_t t_lo = fingerprint ? 0 : p.tree0;
     const int64_t t_hi = fingerprint ? p.n_trees : p.tree0 + p.ntree;
     uint64_t h[DPL];
@@ -1453,7 +1496,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     __syncthreads();  // barrier initialisation visible to every thread
     if (cols_bytes > 0) mbar_wait(bar, 0);
     Acc<U32, DPL> acc;
-    const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_level)
+    const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_flags)
     uint32_t ph0 = 0, ph1 = 0;
     for (int c = c_lo, i = 0; c < c_hi; ++c, ++i) {
         const int b = nbuf == 2 ? (i & 1) : 0;

@@ -8,6 +8,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("ODF_LIB_OVERRIDE"):  # diagnostics / A-B build (tools only)
+    from paper_2205_07307_b200 import odf as _odf
+    _odf.use_library(os.environ["ODF_LIB_OVERRIDE"])
 
 
 def main():
