@@ -62,6 +62,25 @@ int main()
                 if (odf_load_model_ex(&d, &m) != ODF_E_INVALID_ARG) { std::fprintf(stderr, "feature accepted\n"); bad = 1; }
             }
         }
+    // more code columns than TMEM holds (> 512): the TMEM code cache's hot/cold split,
+    // tree classes 0..3 and the class-ordered streams, depths 4..8
+    for (int depth = 4; depth <= 8; ++depth) {
+        const int32_t F = 900;
+        const int64_t T = 700;
+        std::vector<int32_t> fi(T * depth);
+        std::vector<float> thr(T * depth);
+        for (size_t k = 0; k < fi.size(); ++k) {
+            const uint32_t r = rnd() % 1000;  // skewed: low features popular
+            fi[k] = static_cast<int32_t>(r < 500 ? r % 40 : rnd() % F);
+            thr[k] = static_cast<float>(rnd() % 200) / 9.0f;
+        }
+        std::vector<float> lf(T << depth);
+        for (size_t k = 0; k < lf.size(); ++k) lf[k] = static_cast<float>(rnd() % 1000) * 1e-3f;
+        odf_model *m = nullptr;
+        odf_status st = odf_load_model(fi.data(), thr.data(), lf.data(), depth, T, F, 0, &m);
+        if (!valid_status(st)) { std::fprintf(stderr, "wide forest depth %d: %d %s\n", depth, st, odf_last_error()); bad = 1; }
+        if (m) odf_free_model(m);
+    }
     // > 2032 borders on one factor: unsupported
     {
         const int depth = 6;
