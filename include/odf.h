@@ -167,12 +167,6 @@ typedef struct {
                                    for models whose 128-document code block does not fit shared
                                    memory (about > 1,600 code columns, e.g. P:168's 1,950 factors;
                                    at depth 9-10 such widths do not fit at all: ODF_E_UNSUPPORTED) */
-    int32_t tmem_columns;       /* code columns the fused / apply kernels keep in tensor memory (the
-                                   TMEM code cache; 0: shared memory only).  Models
-                                   with such a cache apply their trees in class order (DESIGN.md
-                                   "Summation order"); the order is fixed per model */
-    int32_t tmem_class_chunks[4]; /* tree chunks whose trees read 0, 1, 2 levels from shared memory,
-                                   and chunks read entirely from shared memory */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);

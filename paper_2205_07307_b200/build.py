@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libodf.so")
 # one kernel family per translation unit (odf_kernels.cuh holds the templates), so
 # the objects compile in parallel
 SOURCES = ["odf_capi.cu", "odf_k_fused_nf.cu", "odf_k_fused_nu.cu", "odf_k_fused_wf.cu",
-           "odf_k_fused_wu.cu", "odf_k_apply.cu", "odf_k_halves.cu", "odf_k_t64_f.cu", "odf_k_t64_u.cu", "odf_k_lat_u.cu", "odf_k_tmem.cu",
+           "odf_k_fused_wu.cu", "odf_k_apply.cu", "odf_k_halves.cu", "odf_k_t64_f.cu", "odf_k_t64_u.cu", "odf_k_lat_u.cu",
            "odf_k_aux.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -116,13 +116,6 @@ struct odf_model {
     uint4 *d_fmeta = nullptr;
     float *d_borders = nullptr;
     uint8_t *d_chunks = nullptr;
-    // TMEM code cache (odf_internal.h): the T stream, hot columns, chunk classes, and the
-    // tree order shared by every kernel of the model (null perm: original order)
-    bool tm = false;
-    uint8_t *d_tchunks = nullptr;
-    int32_t n_hot = 0, tcls_end[3] = {0, 0, 0};
-    uint16_t tcol[kTmemCols] = {};
-    int32_t *d_perm = nullptr, *d_iperm = nullptr;
     uint2 *d_splits = nullptr;
     uint2 *d_ucols = nullptr;  // wide models: per used factor {first extra column * 128, C}
     uint2 *d_bchunk = nullptr;
@@ -286,19 +279,7 @@ KParams base_params(const odf_model *m, const Plan &pl)
     for (int sg = 0; sg < m->n_seg; ++sg) p.seg[sg] = m->seg[sg];
     p.half_stride = pl.half_stride;
     p.hdesc_bytes = pl.hdesc_bytes;
-    p.perm = m->d_perm;
-    p.iperm = m->d_iperm;
     return p;
-}
-
-// The fused / apply launch of a 128-document-tile, one-half plan runs the TMEM code
-// cache kernels on the model's T stream when the model has one.
-void use_tmem(const odf_model *m, KParams &p)
-{
-    p.chunks = m->d_tchunks;
-    p.n_hot = m->n_hot;
-    for (int k = 0; k < 3; ++k) p.tcls_end[k] = m->tcls_end[k];
-    memcpy(p.tcol, m->tcol, sizeof p.tcol);
 }
 
 odf_status check_factors_fm(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld)
@@ -399,9 +380,6 @@ void odf_free_model(odf_model *m)
     cudaFree(m->d_fmeta);
     cudaFree(m->d_borders);
     cudaFree(m->d_chunks);
-    cudaFree(m->d_tchunks);
-    cudaFree(m->d_perm);
-    cudaFree(m->d_iperm);
     cudaFree(m->d_splits);
     cudaFree(m->d_ucols);
     cudaFree(m->d_bchunk);
@@ -762,8 +740,7 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
     // ring is as deep as shared memory allows (up to 8 stages: more factor data in
     // flight while phase A runs); at least 16 trees (one per consumer warp)
     const uint32_t unit = kFSubBytes + kMetaBytes + ((m->bord_stride + 15u) & ~15u);
-    std::vector<uint8_t> chunks, tchunks;  // main stream, T stream (TMEM code cache)
-    std::vector<int32_t> tm_perm;          // stream position -> original tree (empty: identity)
+    std::vector<uint8_t> chunks;
     int64_t total_chunk_bytes = 0;
     for (size_t sg = 0; sg < segs.size(); ++sg) {
         const SegSpec &g = segs[sg];
@@ -791,66 +768,21 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         const uint32_t nleaf = 1u << sdepth;
         const float *lf = static_cast<const float *>(g.leaves);
         const uint32_t *lu = static_cast<const uint32_t *>(g.leaves);
-        // level (t, l): its code column and K (bin <= k  <=>  code of column c = k / 127
-        // <= k - 127c)
-        auto level_ck = [&](int64_t t, int l, uint32_t &col, uint32_t &K) {
-            const int32_t f = g.fi[t * sdepth + l];
-            const float thr = g.thr[t * sdepth + l];
-            const auto &b = borders[f];
-            const auto it = std::lower_bound(b.begin(), b.end(), thr, [](float a, float c) { return a < c; });
-            const uint32_t k = static_cast<uint32_t>(it - b.begin());  // b[k] == thr
-            const uint32_t c = k / 127u;
-            col = c == 0 ? static_cast<uint32_t>(used_of[f]) : static_cast<uint32_t>(colB_of[f]) + c - 1u;
-            K = k - 127u * c + 1u;
-        };
-        // ---- TMEM code cache (odf_internal.h): hot columns, tree classes, tree order ----
-        std::vector<int32_t> tidx, tclass, perm;  // per column: TMEM column or -1; per tree: class
-        const bool tm_ok = ODF_TMEM_ENABLED && !u32 && !m->wide && segs.size() == 1 &&
-                           sdepth >= kTmemMinDepth && sdepth <= kTmemMaxDepth && m->n_cols > 0 && g.n_trees > 0;
-        if (tm_ok) {
-            std::vector<int64_t> uses(m->n_cols, 0);
-            std::vector<uint32_t> lcol(static_cast<size_t>(g.n_trees) * sdepth);
-            for (int64_t t = 0; t < g.n_trees; ++t)
-                for (int l = 0; l < sdepth; ++l) {
-                    uint32_t col, K;
-                    level_ck(t, l, col, K);
-                    lcol[t * sdepth + l] = col;
-                    ++uses[col];
-                }
-            // the kTmemCols most used columns (ties: lower column), in column order
-            std::vector<int32_t> order(m->n_cols);
-            for (int32_t c = 0; c < m->n_cols; ++c) order[c] = c;
-            std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t c) { return uses[a] > uses[c]; });
-            const int32_t nh = std::min<int32_t>(m->n_cols, kTmemCols);
-            std::sort(order.begin(), order.begin() + nh);
-            tidx.assign(m->n_cols, -1);
-            for (int32_t k = 0; k < nh; ++k) {
-                tidx[order[k]] = k;
-                m->tcol[k] = static_cast<uint16_t>(order[k]);
-            }
-            m->n_hot = (nh + 3) & ~3;  // padded entries copy column 0 (never read)
-            tclass.resize(g.n_trees);
-            for (int64_t t = 0; t < g.n_trees; ++t) {
-                int cold = 0;
-                for (int l = 0; l < sdepth; ++l) cold += tidx[lcol[t * sdepth + l]] < 0;
-                tclass[t] = std::min(cold, 3);
-            }
-            // stable partition by class: the order every kernel of this model applies trees in
-            perm.resize(g.n_trees);
-            for (int64_t t = 0; t < g.n_trees; ++t) perm[t] = static_cast<int32_t>(t);
-            std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t c) { return tclass[a] < tclass[c]; });
-            bool identity = true;
-            for (int64_t t = 0; t < g.n_trees && identity; ++t) identity = perm[t] == t;
-            if (identity) perm.clear();
-        }
-        for (int64_t pos = 0; pos < g.n_trees; ++pos) {
-            const int64_t t = perm.empty() ? pos : perm[pos];  // stream position -> original tree
-            uint8_t *ch = chunks.data() + base + static_cast<size_t>(pos / tc) * cbytes;
-            const int64_t i = pos % tc;
+        for (int64_t t = 0; t < g.n_trees; ++t) {
+            uint8_t *ch = chunks.data() + base + static_cast<size_t>(t / tc) * cbytes;
+            const int64_t i = t % tc;
             uint32_t *desc = reinterpret_cast<uint32_t *>(ch + i * dstride);
             for (int l = 0; l < sdepth; ++l) {
-                uint32_t col, K;
-                level_ck(t, l, col, K);
+                const int32_t f = g.fi[t * sdepth + l];
+                const float thr = g.thr[t * sdepth + l];
+                const auto &b = borders[f];
+                const auto it = std::lower_bound(b.begin(), b.end(), thr, [](float a, float c) { return a < c; });
+                const uint32_t k = static_cast<uint32_t>(it - b.begin());  // b[k] == thr
+                // bin <= k  <=>  code of column c = k / 127 <= k - 127c
+                const uint32_t c = k / 127u;
+                const uint32_t col = c == 0 ? static_cast<uint32_t>(used_of[f])
+                                            : static_cast<uint32_t>(colB_of[f]) + c - 1u;
+                const uint32_t K = k - 127u * c + 1u;
                 if (desc_fmt(sdepth) == DESC_SPLIT) {
                     desc[l] = col * kTile;
                     desc[sdepth + l / 4] |= (128u - K) << (8 * (l % 4));
@@ -869,51 +801,6 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
                 else
                     reinterpret_cast<float *>(tab)[leaf_pos(sdepth, F)] = lf[src];
             }
-        }
-        if (tm_ok) {
-            // ---- the T stream: a copy of the main stream whose chunks of class <= 2 hold
-            //      T-format trees (levels permuted: D - C TMEM levels first) ----
-            tchunks.assign(chunks.begin() + base, chunks.end());
-            for (int32_t c = 0; c < nch; ++c) {
-                const int64_t last = std::min<int64_t>((c + 1) * static_cast<int64_t>(tc), g.n_trees) - 1;
-                const int C = tclass[perm.empty() ? last : perm[last]];  // the chunk's class
-                for (int k = C; k < 3; ++k) m->tcls_end[k] = c + 1;
-                if (C == 3) continue;  // split format, as in the main stream
-                uint8_t *ch = tchunks.data() + static_cast<size_t>(c) * cbytes;
-                for (int64_t pos = c * static_cast<int64_t>(tc); pos <= last; ++pos) {
-                    const int64_t t = perm.empty() ? pos : perm[pos];
-                    const int64_t i = pos % tc;
-                    uint32_t col[kTmemMaxDepth], K[kTmemMaxDepth];
-                    int ord[kTmemMaxDepth], n = 0;
-                    for (int l = 0; l < sdepth; ++l) level_ck(t, l, col[l], K[l]);
-                    for (int l = 0; l < sdepth; ++l)  // hot levels first (original order), then cold
-                        if (tidx[col[l]] >= 0) ord[n++] = l;
-                    for (int l = 0; l < sdepth; ++l)
-                        if (tidx[col[l]] < 0) ord[n++] = l;
-                    const int NT = sdepth - C;  // TMEM levels; a tree with fewer cold levels
-                                                // reads its last hot ones from shared memory
-                    uint32_t *desc = reinterpret_cast<uint32_t *>(ch + i * dstride);
-                    std::fill(desc, desc + 8, 0u);
-                    for (int l = 0; l < sdepth; ++l) {
-                        const int o = ord[l];
-                        if (l < NT)
-                            desc[l / 2] |= static_cast<uint32_t>(tidx[col[o]]) << (16 * (l % 2));
-                        else
-                            desc[6 + (l - NT)] = col[o] * kTile;
-                        desc[4 + l / 4] |= (128u - K[o]) << (8 * (l % 4));
-                    }
-                    // table: new level l is original level ord[l]; F' = complement of the
-                    // new index I', and the answer is the original leaf of index I
-                    uint8_t *tab = ch + dbytes + i * tstride;
-                    for (uint32_t F = 0; F < nleaf; ++F) {
-                        const uint32_t Ip = nleaf - 1 - F;
-                        uint32_t I = 0;
-                        for (int l = 0; l < sdepth; ++l) I |= ((Ip >> l) & 1u) << ord[l];
-                        reinterpret_cast<float *>(tab)[leaf_pos(sdepth, F)] = lf[static_cast<size_t>(t) * nleaf + I];
-                    }
-                }
-            }
-            tm_perm.swap(perm);
         }
         if (sg == 0) {  // the uniform geometry (a mixed model's slot is sized below)
             m->tc = tc;
@@ -937,27 +824,13 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
     std::vector<uint32_t> bits_desc;
     if (!u32 && segs.size() == 1) {
         bits_desc.resize(static_cast<size_t>(n_nodes));
-        const int D0 = segs[0].depth;
-        for (int64_t kk = 0; kk < n_nodes; ++kk) {  // stream order (tm_perm): the kernels' tree order
-            const int64_t k = tm_perm.empty() ? kk : tm_perm[kk / D0] * static_cast<int64_t>(D0) + kk % D0;
+        for (int64_t k = 0; k < n_nodes; ++k) {
             const int32_t f = feature_index[k];
             const auto &b = borders[f];
             const uint32_t j = static_cast<uint32_t>(
                 std::lower_bound(b.begin(), b.end(), thresholds[k], [](float a, float c) { return a < c; }) -
                 b.begin());
-            bits_desc[kk] = (bf_base[used_of[f]] + j) * 4u;
-        }
-    }
-    // answers in stream order for the bit-word apply (NEXT-3); inverse order for K6
-    std::vector<float> leaves_s;
-    std::vector<int32_t> tm_iperm;
-    if (!tm_perm.empty()) {
-        const size_t nl = size_t(1) << segs[0].depth;
-        leaves_s.resize(static_cast<size_t>(n_leaves));
-        tm_iperm.resize(tm_perm.size());
-        for (size_t pos = 0; pos < tm_perm.size(); ++pos) {
-            std::memcpy(leaves_s.data() + pos * nl, leaf_f + static_cast<size_t>(tm_perm[pos]) * nl, nl * 4);
-            tm_iperm[tm_perm[pos]] = static_cast<int32_t>(pos);
+            bits_desc[k] = (bf_base[used_of[f]] + j) * 4u;
         }
     }
 
@@ -992,11 +865,7 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         (e = up(reinterpret_cast<void **>(&m->d_bchunk), bchunk.data(), bchunk.size() * sizeof(uint2))) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_bf_base), bf_base.data(), bf_base.size() * 4)) != cudaSuccess ||
         (e = up(reinterpret_cast<void **>(&m->d_bits_desc), bits_desc.data(), bits_desc.size() * 4)) != cudaSuccess ||
-        (e = up(reinterpret_cast<void **>(&m->d_leaves), leaves_s.empty() ? leaf_values : leaves_s.data(),
-                u32 ? 0 : static_cast<size_t>(n_leaves) * 4)) != cudaSuccess ||
-        (e = up(reinterpret_cast<void **>(&m->d_tchunks), tchunks.data(), tchunks.size())) != cudaSuccess ||
-        (e = up(reinterpret_cast<void **>(&m->d_perm), tm_perm.data(), tm_perm.size() * 4)) != cudaSuccess ||
-        (e = up(reinterpret_cast<void **>(&m->d_iperm), tm_iperm.data(), tm_iperm.size() * 4)) != cudaSuccess) {
+        (e = up(reinterpret_cast<void **>(&m->d_leaves), leaf_values, u32 ? 0 : static_cast<size_t>(n_leaves) * 4)) != cudaSuccess) {
         odf_model *raw = m.release();
         odf_free_model(raw);
         return e == cudaErrorMemoryAllocation ? fail(ODF_E_NOMEM, "device allocation failed")
@@ -1022,9 +891,6 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         return fail(ODF_E_UNSUPPORTED, "%s", why.c_str());
     }
     m->binz.grid_per_sm = occupancy_main(MODE_BINARIZE, 0, m->binz.smem, m->tile_docs);
-    // the TMEM code cache runs with the 128-document-tile plans (one CTA per SM: all 512
-    // TMEM columns)
-    m->tm = m->d_tchunks != nullptr && m->tile_docs == kTile;
     // 256-document tiles (two halves), fp32 narrow models, when two code blocks fit
     if (!m->leaf_u32 && !m->wide && m->tile_docs == kTile) {
         std::string why2;
@@ -1067,10 +933,6 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->bins_tile_docs = m->tile_docs;
     info->stages_fused_256 = m->fused2.valid ? m->fused2.stages : 0;
     info->smem_fused_256 = m->fused2.valid ? static_cast<int32_t>(m->fused2.smem) : 0;
-    info->tmem_columns = m->tm ? m->n_hot : 0;
-    for (int k = 0; k < 4; ++k)
-        info->tmem_class_chunks[k] = !m->tm ? 0
-                                     : (k < 3 ? m->tcls_end[k] : m->n_tchunks) - (k > 0 ? m->tcls_end[k - 1] : 0);
     return ok();
 }
 
@@ -1095,7 +957,6 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     const Plan &pl = halves == 2 ? (mode == MODE_FUSED ? m->fused2 : m->apply2)
                                  : mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
     KParams p = base_params(m, pl);
-    if (m->tm && halves == 1 && mode != MODE_BINARIZE) use_tmem(m, p);
     p.n_docs = n_docs;
     p.n_tiles = (n_docs + m->tile_docs * halves - 1) / (m->tile_docs * halves);
     p.bins_in = bins_in;

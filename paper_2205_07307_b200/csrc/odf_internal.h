@@ -64,30 +64,6 @@ __host__ __device__ constexpr int trees_per_chunk(int depth)
 
 enum Mode : int { MODE_FUSED = 0, MODE_BINARIZE = 1, MODE_APPLY = 2 };
 
-// TMEM code cache (fused / apply kernels; fp32 narrow models of uniform depth 4..8 with
-// 128-document tiles).  After phase A each of the 4 sub-partitions' TMEM
-// lanes gets a copy of the tile's hot code columns (lane 32q + j = documents 4j..4j+3,
-// TMEM column t = hot column t), so most per-level code-word loads (tcgen05.ld) leave
-// the shared-memory data path.  The forest is compiled a second time for these kernels
-// (the "T stream", same chunk geometry and tree order as the main stream): a tree's
-// class C = its number of levels on cold columns (C <= 2; C = 3: more).  Trees are
-// applied in class order (a stable partition, identical in every kernel of the model),
-// each chunk runs the class of its last tree, and its trees are written in that class's
-// format:
-//  * C <= 2, "T format" (32 B): levels permuted so the D - C TMEM levels come first
-//    (the leaf table permuted to match); words 0-3: u16 TMEM columns of levels
-//    0..D-C-1 (level i in halfword i); words 4-5: the (128 - K) bytes of all levels
-//    (level i in byte i % 4 of word 4 + i / 4); words 6-7: col * 128 of the shared-
-//    memory levels D-C, D-C+1;
-//  * C = 3: the main stream's split format (every level from shared memory).
-#ifdef ODF_NO_TMEM  // A/B builds only (paper_2205_07307_b200.build.build_variant)
-#define ODF_TMEM_ENABLED false
-#else
-#define ODF_TMEM_ENABLED true
-#endif
-constexpr int kTmemCols = 512;
-constexpr int kTmemMinDepth = 4, kTmemMaxDepth = 8;
-
 // Mixed-height models (NEXT-2, the paper's native layout): the forest is a
 // list of height segments, each with its own tree-chunk geometry, concatenated in
 // one chunk stream; kernels instantiated with DEPTH = kMixedDepth apply each chunk
@@ -159,13 +135,7 @@ struct KParams {
     uint32_t *words;           // [ceil(D/32)][k_bin]
     const uint32_t *bits_desc; // [n_trees][depth] byte offset (kb * 4) of each level's word
     const float *leaves;       // [n_trees << depth] original leaf order
-    // ---- TMEM code cache (the T stream in `chunks`; n_hot = 0: shared memory only) ----
-    int32_t n_hot;                  // hot columns held in tensor memory, a multiple of 4
-    int32_t tcls_end[3];            // chunks [0, e0): class 0, [e0, e1): 1, [e1, e2): 2, rest: 3
-    uint16_t tcol[kTmemCols];       // TMEM column t <- code column tcol[t]
     // ---- index export / fingerprint ----
-    const int32_t *perm;            // stream position -> original tree (null: identity)
-    const int32_t *iperm;           // original tree -> stream position (null: identity)
     int64_t doc0, ndoc, tree0, ntree;
     uint16_t *idx_out;
     uint64_t *fp_out;
@@ -188,7 +158,6 @@ const void *kptr_lat_u(int depth, int tile_docs);  // K4 apply, u32 leaves: dept
 const void *kptr_fused_h2(int depth);  // fused, fp32 leaves, 256-document tiles (H = 2)
 const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);
-const void *kptr_tmem(int mode, int depth);  // TMEM code cache: fused / apply, fp32, depth 4..8
 
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s, int halves = 1);  // p.tile_docs picks DPL

@@ -35,10 +35,8 @@ cudaError_t launch_bits(int depth, const KParams &p, bool apply, size_t smem, cu
 // dispatch
 // ---------------------------------------------------------------------------
 static const void *main_kernel(int mode, int depth, bool u32 = false, bool wide = false, int halves = 1,
-                               int tile_docs = 128, bool tm = false)
+                               int tile_docs = 128)
 {
-    if (tm)  // TMEM code cache: fp32 narrow models, 128-document tiles, one half
-        return (!u32 && !wide && halves == 1 && tile_docs == 128) ? kptr_tmem(mode, depth) : nullptr;
     if (tile_docs == 64) {  // 64-document tiles: narrow models, one half
         if (wide || halves != 1) return nullptr;
         if (mode == MODE_BINARIZE) return kptr_t64_f(MODE_BINARIZE, 0);  // bins: leaf type irrelevant
@@ -154,11 +152,6 @@ cudaError_t prepare_kernels(int max_smem)
             if (e != cudaSuccess) return e;
         }
     }
-    for (int d = kTmemMinDepth; d <= kTmemMaxDepth; ++d)
-        for (int mode : {MODE_FUSED, MODE_APPLY}) {
-            cudaError_t e = opt_in(kptr_tmem(mode, d), max_smem);
-            if (e != cudaSuccess) return e;
-        }
     for (int d = 0; d <= kMixedDepth; ++d)
         for (int td : {128, 64}) {
             cudaError_t e = opt_in(lat_apply_kernel(d, td, true), max_smem);
@@ -194,7 +187,7 @@ int occupancy_main(int mode, int depth, size_t smem, int tile_docs)
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
                         size_t smem, cudaStream_t s, int halves)
 {
-    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0, halves, p.tile_docs, p.n_hot > 0);
+    const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0, halves, p.tile_docs);
     if (!f) return cudaErrorInvalidValue;
     KParams pc = p;
     CUtensorMap tm;

@@ -887,123 +887,6 @@ __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes,
     }
 }
 
-// ---------------------------------------------------------------------------
-// TMEM code cache (odf_internal.h "TMEM code cache").  sm_100a tensor
-// memory is 128 lanes x 512 columns x 32 bit per SM; a warp reads the 32 lanes of its
-// sub-partition (warp & 3) with tcgen05.ld.  Lane 32q + j, column t holds the u32 code
-// word of documents 4j..4j+3 for hot column t (the layout of one shared-memory code
-// row), replicated in all four sub-partitions.  Reading a level's code word from TMEM
-// instead of shared memory takes it off the 128 B/clk shared-memory data path, which
-// binds the apply phase (profiles/README.md).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void tm_alloc(uint32_t dst_off)  // one warp; address -> shared [dst_off]
-{
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sabs(dst_off)),
-                 "n"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tm_dealloc(uint32_t taddr)
-{
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kTmemCols) : "memory");
-}
-__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// one 32-bit column of the warp's 32 lanes (asynchronous: the register is defined only
-// after tm_wait_ld, and tm_tie keeps every use after that wait)
-__device__ __forceinline__ uint32_t tm_ld(uint32_t taddr)
-{
-    uint32_t r;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
-    return r;
-}
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tm_tie(uint32_t &r) { asm volatile("" : "+r"(r)); }
-__device__ __forceinline__ void tm_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a), "r"(b),
-                 "r"(c), "r"(d)
-                 : "memory");
-}
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// Copy the tile's hot code rows (shared memory) into the warp's sub-partition: the 4
-// warps of a sub-partition copy every 4th group of 4 columns (p.n_hot is a multiple of 4).
-__device__ __forceinline__ void tm_fill(const KParams &p, const Lane &ln, uint32_t tbase, int warp)
-{
-#pragma unroll 1
-    for (int t = (warp >> 2) * 4; t < p.n_hot; t += 16) {
-        const uint32_t a = ldsa_u32(ln.bins + (static_cast<uint32_t>(p.tcol[t]) << 7));
-        const uint32_t b = ldsa_u32(ln.bins + (static_cast<uint32_t>(p.tcol[t + 1]) << 7));
-        const uint32_t c = ldsa_u32(ln.bins + (static_cast<uint32_t>(p.tcol[t + 2]) << 7));
-        const uint32_t d = ldsa_u32(ln.bins + (static_cast<uint32_t>(p.tcol[t + 3]) << 7));
-        tm_st4(tbase + static_cast<uint32_t>(t), a, b, c, d);
-    }
-}
-
-// G trees of one T-format chunk of class C (trees i0, i0 + 16, ...: one group's trees in
-// ascending order): descriptors, then every TMEM load and shared-memory level of the G
-// trees, one wait, then flags, leaf addresses and gathers tree by tree.
-template <int DEPTH, int C, int G>
-__device__ __forceinline__ void apply_group_tm(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
-                                               uint32_t tbase, int i0, Acc<false, 4> &acc)
-{
-    constexpr int NT = DEPTH - C;  // TMEM levels (first), then C shared-memory levels
-    uint4 q0[G], q1[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const uint32_t d = chunk + (i0 + g * kConsumerWarps) * desc_stride(DEPTH);
-        q0[g] = lds_v4u(d);
-        q1[g] = lds_v4u(d + 16);
-    }
-    uint32_t w[G][DEPTH];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const uint32_t cw[4] = {q0[g].x, q0[g].y, q0[g].z, q0[g].w};
-        // TMEM address = lane field of tbase | the level's u16 column: one PRMT
-#pragma unroll
-        for (int l = 0; l < NT; ++l) w[g][l] = tm_ld(__byte_perm(cw[l >> 1], tbase, (l & 1) ? 0x7632u : 0x7610u));
-        if constexpr (C >= 1) w[g][NT] = code_word<4>(ln.bins + q1[g].z);
-        if constexpr (C >= 2) w[g][NT + 1] = code_word<4>(ln.bins + q1[g].w);
-    }
-    tm_wait_ld();
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int l = 0; l < NT; ++l) tm_tie(w[g][l]);
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const uint32_t kw[2] = {q1[g].x, q1[g].y};
-        uint32_t f[DEPTH];
-#pragma unroll
-        for (int l = 0; l < DEPTH; ++l) f[l] = (w[g][l] + __byte_perm(kw[l >> 2], 0u, 0x1111u * (l & 3))) & 0x80808080u;
-        const uint32_t lo = merge_flags<DEPTH>(f);
-        const uint32_t tb = sabs(chunk + desc_bytes + (i0 + g * kConsumerWarps) * table_stride(DEPTH));
-        uint32_t a[4];
-        addrs_from_flags<DEPTH, 4>(lo, 0u, tb, a);
-        acc.add4(a);
-    }
-}
-
-template <int DEPTH, int C>
-__device__ __forceinline__ void apply_chunk_tm(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
-                                               uint32_t tbase, int warp, int nk, Acc<false, 4> &acc)
-{
-    if ((nk & 3) == 0) {
-#pragma unroll 1
-        for (int k = 0; k < nk; k += 4)
-            apply_group_tm<DEPTH, C, 4>(chunk, desc_bytes, ln, tbase, warp + k * kConsumerWarps, acc);
-    } else if ((nk & 1) == 0) {
-#pragma unroll 1
-        for (int k = 0; k < nk; k += 2)
-            apply_group_tm<DEPTH, C, 2>(chunk, desc_bytes, ln, tbase, warp + k * kConsumerWarps, acc);
-    } else {
-#pragma unroll 1
-        for (int k = 0; k < nk; ++k)
-            apply_group_tm<DEPTH, C, 1>(chunk, desc_bytes, ln, tbase, warp + k * kConsumerWarps, acc);
-    }
-}
-
 // Fixed-order combine of the 16 group partials of document tid (< tile_docs) and store:
 // score = (((P_0 + P_1) + P_2) + ... + P_15).
 template <int DPL>
@@ -1146,8 +1029,7 @@ __device__ __forceinline__ int valid_halves(int64_t n_docs, int64_t tile)
     return v < H ? static_cast<int>(v) : H;
 }
 
-// TM: TMEM code cache (p.chunks is the model's T stream, p.n_hot > 0).
-template <int MODE, int DEPTH, bool U32, bool WIDE, int H = 1, int DPL = 4, bool TM = false>
+template <int MODE, int DEPTH, bool U32, bool WIDE, int H = 1, int DPL = 4>
 __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K1: 2 CTAs per SM
     odf_main_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -1161,9 +1043,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
     static_assert(!MIXED || (H == 1 && U32), "mixed-height models: integer answers, 128-doc tiles");
     static_assert(DPL == 4 || (DPL == 2 && H == 1 && !WIDE), "64-document tiles: narrow models, one half");
     static_assert(H == 1 || (H == 2 && !WIDE && MODE != MODE_BINARIZE), "halves: fused/apply, narrow");
-    static_assert(!TM || (DEPTH >= kTmemMinDepth && DEPTH <= kTmemMaxDepth && !U32 && !WIDE && H == 1 &&
-                          DPL == 4 && MODE != MODE_BINARIZE),
-                  "TMEM code cache: fp32 narrow fused / apply, 128-document tiles, depth 4..8");
     if (smem_addr(smem_raw) & 1023u) __trap();  // alignment the TMA swizzle relies on
     const uint32_t base = 0;
     const uint32_t bins = base + p.off_bins;
@@ -1195,11 +1074,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
     }
     if (HAS_A)
         for (int c = threadIdx.x; c < p.n_fchunks; c += kThreads) sst<uint2>(bct + 8u * c, p.bchunk[c]);
-    const uint32_t tm_addr_off = bars + 152u;  // the TMEM address (written by tcgen05.alloc)
-    if (TM && warp == 0) tm_alloc(tm_addr_off);
-    if (TM) tm_fence_before();
     __syncthreads();
-    if (TM) tm_fence_after();
 
     if (warp == kConsumerWarps) {
         // ===================== producer warp (one elected lane) =====================
@@ -1289,10 +1164,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
     const Lane ln = make_lane(p, sabs(bins + half * p.half_stride) + lane * DPL);  // absolute (tree_flags)
     const uint32_t desc_off = H == 1 ? p.desc_bytes : p.hdesc_bytes;  // tables in a ring slot
     const int nk = H == 1 ? p.tc / kConsumerWarps : p.tc / (2 * kSlots);  // trees per job per warp
-    // TMEM: this warp's sub-partition lanes 32 * (warp & 3) (address: lane << 16 | column)
-    const uint32_t tm_base = TM ? sld<uint32_t>(tm_addr_off) : 0u;
-    if (TM && (tm_base & 0xffffu)) __trap();  // all 512 columns: column field 0 (T-format PRMT)
-    const uint32_t tbase = tm_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
     uint32_t slot = 0, ph = 0, bph = 0;
 #if ODF_DIAG & 8
     int diag_it = 0;
@@ -1342,13 +1213,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         }
         DIAG_T(t_adone);
         named_bar_consumers();  // all bins of the tile written
-        if constexpr (TM) {     // hot code rows -> every sub-partition's TMEM lanes
-            tm_fill(p, ln, tbase, warp);
-            tm_wait_st();
-            tm_fence_before();
-            named_bar_consumers();
-            tm_fence_after();
-        }
         DIAG_T(t_bstart);
 
         // acc: the group of the warp's next tree; acc2 (H = 2): the other group
@@ -1394,13 +1258,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
 #endif
             {
                 if constexpr (MIXED) {
-                } else if constexpr (TM) {
-                    // chunk class (warp-uniform): T format with 0..2 shared-memory levels, or split format
-                    const int cls = c < p.tcls_end[0] ? 0 : c < p.tcls_end[1] ? 1 : c < p.tcls_end[2] ? 2 : 3;
-                    if (cls == 0) apply_chunk_tm<DEPTH, 0>(sb, desc_off, ln, tbase, tslot, nk, acc);
-                    else if (cls == 1) apply_chunk_tm<DEPTH, 1>(sb, desc_off, ln, tbase, tslot, nk, acc);
-                    else if (cls == 2) apply_chunk_tm<DEPTH, 2>(sb, desc_off, ln, tbase, tslot, nk, acc);
-                    else apply_chunk<DEPTH, U32, DPL>(sb, desc_off, ln, tslot, nk, acc);
                 } else if constexpr (H == 1) {
                     apply_chunk<DEPTH, U32, DPL>(sb, desc_off, ln, tslot, nk, acc);
                 } else {
@@ -1421,10 +1278,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         }
         DIAG_T(t_bdone);
         // reduction buffer aliases the bins: wait until every warp is done with them
-        // (and, TM, with the TMEM columns the next tile's fill overwrites)
-        if (TM) tm_fence_before();
         named_bar_consumers();
-        if (TM) tm_fence_after();
         // a warp applies an even number of trees per tile (tc is a multiple of 16), so
         // acc holds group tslot and acc2 group tslot + 8 (H = 2)
         acc.to_red(red, tslot, half * kT + lane * DPL, kTileH);
@@ -1445,12 +1299,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         }
         ++diag_it;
 #endif
-    }
-    if constexpr (TM) {  // every consumer warp is past its last TMEM access
-        tm_fence_before();
-        named_bar_consumers();
-        tm_fence_after();
-        if (warp == 0) tm_dealloc(tm_base);
     }
 }
 
@@ -1483,34 +1331,11 @@ __global__ void __launch_bounds__(kConsumerThreads)
         __syncthreads();
     }
     const Lane ln = make_lane(p, sabs(bins) + lane * DPL);  // absolute (tree_flags)
-    // stream positions to visit: a reordered forest (p.perm, odf_internal.h "TMEM code
-    // cache") exports by original tree index, so every position is visited
-    const int64_t t_lo = (fingerprint || p.perm) ? 0 : p.tree0;
-    const int64_t t_hi = (fingerprint || p.perm) ? p.n_trees : p.tree0 + p.ntree;
+    const int64_t t_lo = fingerprint ? 0 : p.tree0;
+    const int64_t t_hi = fingerprint ? p.n_trees : p.tree0 + p.ntree;
     uint64_t h[DPL];
 #pragma unroll
     for (int n = 0; n < DPL; ++n) h[n] = 0xcbf29ce484222325ull;
-    if (fingerprint && p.iperm) {  // hash in ORIGINAL tree order: one tree's descriptors at a time
-        if (warp == 0) {
-            constexpr uint32_t ds = desc_stride(DEPTH);
-            for (int64_t t = 0; t < p.n_trees; ++t) {
-                const int64_t pos = p.iperm[t];
-                const uint8_t *src = p.chunks + static_cast<size_t>(pos / p.tc) * p.chunk_bytes + (pos % p.tc) * ds;
-                if (lane < static_cast<int>(ds / 16))
-                    sts_v4u(descs + 16 * lane, __ldg(reinterpret_cast<const uint4 *>(src) + lane));
-                __syncwarp();
-                uint32_t F[DPL];
-                tree_findex<DEPTH, DPL>(descs, ln, F);
-                __syncwarp();
-#pragma unroll
-                for (int n = 0; n < DPL; ++n) {
-                    const uint32_t idx = F[n] ^ ((1u << DEPTH) - 1u);
-                    h[n] = (h[n] ^ (idx & 0xffu)) * 0x100000001b3ull;
-                    h[n] = (h[n] ^ (idx >> 8)) * 0x100000001b3ull;
-                }
-            }
-        }
-    } else
     for (int64_t c = t_lo / p.tc; c * p.tc < t_hi; ++c) {
         const uint8_t *chunk = p.chunks + static_cast<size_t>(c) * p.chunk_bytes;
         const uint32_t dbytes = static_cast<uint32_t>(p.tc) * desc_stride(DEPTH);
@@ -1533,9 +1358,8 @@ __global__ void __launch_bounds__(kConsumerThreads)
             }
         } else {
             for (int i = warp; i < p.tc; i += kConsumerWarps) {
-                if (c0 + i >= p.n_trees) continue;
-                const int64_t t = p.perm ? p.perm[c0 + i] : c0 + i;  // original tree index
-                if (t < p.tree0 || t >= p.tree0 + p.ntree) continue;
+                const int64_t t = c0 + i;
+                if (t < p.tree0 || t >= t_hi) continue;
                 uint32_t F[DPL];
                 tree_findex<DEPTH, DPL>(descs + i * desc_stride(DEPTH), ln, F);
 #pragma unroll

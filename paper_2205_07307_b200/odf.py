@@ -43,8 +43,7 @@ class _Info(ctypes.Structure):
                 ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32),
                 ("bins_elem_bytes", ctypes.c_int32), ("max_tile_docs", ctypes.c_int32),
                 ("stages_fused_256", ctypes.c_int32), ("smem_fused_256", ctypes.c_int32),
-                ("bins_tile_docs", ctypes.c_int32), ("tmem_columns", ctypes.c_int32),
-                ("tmem_class_chunks", ctypes.c_int32 * 4)]
+                ("bins_tile_docs", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
@@ -244,7 +243,6 @@ class Model:
         inf = _Info()
         _check(L.odf_get_info(self._h, ctypes.byref(inf)))
         self.info = {k: getattr(inf, k) for k, _ in _Info._fields_}
-        self.info["tmem_class_chunks"] = list(self.info["tmem_class_chunks"])
         self.depth = int(inf.depth)
         self.n_trees = int(inf.n_trees)
         self.n_features = int(inf.n_features)

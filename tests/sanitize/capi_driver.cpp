@@ -62,8 +62,7 @@ int main()
                 if (odf_load_model_ex(&d, &m) != ODF_E_INVALID_ARG) { std::fprintf(stderr, "feature accepted\n"); bad = 1; }
             }
         }
-    // more code columns than TMEM holds (> 512): the TMEM code cache's hot/cold split,
-    // tree classes 0..3 and the class-ordered streams, depths 4..8
+    // many code columns (> 512) with skewed usage, depths 4..8
     for (int depth = 4; depth <= 8; ++depth) {
         const int32_t F = 900;
         const int64_t T = 700;

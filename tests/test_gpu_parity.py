@@ -811,8 +811,8 @@ def test_condition_words_and_bits_apply(name, n_docs, n_trees):
 
 
 # ---------------------------------------------------------------------------
-# TMEM code cache (odf_internal.h): models with more code columns than
-# tensor memory holds apply their trees in class order with permuted levels
+# Many code columns (more than tensor memory would hold: the round-2 TMEM code-cache
+# experiment, profiles/r2_tmem_experiment.json) with skewed column usage
 # ---------------------------------------------------------------------------
 def _many_column_case(depth, n_docs=3000, n_trees=700, n_features=900, seed=41, exact=True):
     rng = np.random.default_rng(seed + depth)
@@ -823,25 +823,20 @@ def _many_column_case(depth, n_docs=3000, n_trees=700, n_features=900, seed=41, 
                   rng.integers(0, n_features, n_trees * depth)).astype(np.int32)
     thr = pools[fi, rng.integers(0, 24, fi.size)].astype(np.float32)
     lv = synth.leaves(seed, n_trees, depth, 0.01, exact=exact)
-    return synth.ForestCase("tmem", x, n_features, fi, thr, lv, depth, n_trees)
+    return synth.ForestCase("many-columns", x, n_features, fi, thr, lv, depth, n_trees)
 
 
 @pytest.mark.parametrize("depth", [4, 5, 6, 7, 8])
-def test_tmem_code_cache_every_class(depth):
-    """Hot columns in TMEM, cold ones in shared memory: chunks of every class (0, 1, 2
-    shared-memory levels, and all levels from shared memory) are applied; with
-    exact-arithmetic leaves the fused and two-stage scores are bit-exact against the
-    oracle, bins / fingerprints / the leaf-index export (by original tree index) are
-    exact, and the bit-word apply and the latency path agree bit for bit."""
+def test_many_columns_exact(depth):
+    """> 512 code columns, skewed usage: with exact-arithmetic leaves the fused and
+    two-stage scores are bit-exact against the oracle, bins / fingerprints / the full
+    leaf-index export are exact, and the bit-word apply and the latency path agree bit
+    for bit."""
     import torch
     case = _many_column_case(depth)
-    m = cuda_model(case)
-    info = m.info
-    assert info["tmem_columns"] == 512 and info["n_columns"] > 512, info
-    assert sum(1 for k in info["tmem_class_chunks"] if k > 0) >= 3, info["tmem_class_chunks"]
-    m.close()
     f = full_check(case, exact=True, idx_window=(0, case.n_docs, 0, case.n_trees))
     m = cuda_model(case)
+    assert m.info["n_columns"] > 512, m.info
     x = to_dev(case.x)
     bins = m.binarize(x)
     s_bits = m.apply_bits(m.bits_from_bins(bins, case.n_docs), case.n_docs).cpu().numpy()
@@ -853,8 +848,8 @@ def test_tmem_code_cache_every_class(depth):
 
 
 @pytest.mark.parametrize("n_docs", [1, 129, 5000])
-def test_tmem_code_cache_fp32_tolerance(n_docs):
+def test_many_columns_fp32_tolerance(n_docs):
     """fp32 leaves on a many-column model: scores within the tolerance, fused ==
-    two-stage bit for bit, batch-independent."""
+    two-stage bit for bit."""
     case = _many_column_case(6, n_docs=n_docs, exact=False)
     full_check(case)
