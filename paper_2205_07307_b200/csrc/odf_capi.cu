@@ -748,7 +748,11 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         const int dstride = desc_stride(sdepth);
         const uint32_t tstride = static_cast<uint32_t>(table_stride(sdepth));
         const uint32_t per = static_cast<uint32_t>(dstride) + tstride;
-        const int32_t tc = 16 * static_cast<int32_t>(std::max<uint32_t>(1u, unit / (16u * per)));
+#ifndef ODF_TC_MULT
+#define ODF_TC_MULT 16  // A/B builds only: trees per chunk rounded to this multiple
+#endif
+        const uint32_t tcm = (sdepth <= 6) ? ODF_TC_MULT : 16u;
+        const int32_t tc = static_cast<int32_t>(tcm * std::max<uint32_t>(1u, unit / (tcm * per)));
         const uint32_t dbytes = align_up(static_cast<uint64_t>(tc) * dstride, 256);
         const uint32_t cbytes = dbytes + static_cast<uint32_t>(tc) * tstride;
         const int32_t nch = static_cast<int32_t>((g.n_trees + tc - 1) / tc);

@@ -847,9 +847,6 @@ struct Acc<true, DPL> {
 #ifndef ODF_APPLY_UNROLL
 #define ODF_APPLY_UNROLL 2
 #endif
-#ifndef ODF_UNROLL3
-#define ODF_UNROLL3 0  // 3 trees per iteration when a warp's trees per chunk are a multiple of 3 (A/B)
-#endif
 constexpr int kApplyUnroll = ODF_APPLY_UNROLL;  // trees in flight per warp
 
 template <int DEPTH, bool U32, int DPL = 4>
@@ -865,6 +862,17 @@ __device__ __forceinline__ void apply_tree(uint32_t chunk, uint32_t desc_bytes, 
     acc.add4(a);
 }
 
+// All NK trees of the warp in one unrolled block: ptxas schedules the whole chunk
+// (descriptor, code-word and gather loads of every tree in flight together) instead
+// of one loop iteration at a time (c3, 6 trees per warp: fused 6.37 -> 6.14 ms).
+template <int DEPTH, bool U32, int DPL, int NK>
+__device__ __forceinline__ void apply_trees_all(uint32_t chunk, uint32_t desc_bytes, const Lane &ln, int warp,
+                                                Acc<U32, DPL> &acc)
+{
+#pragma unroll
+    for (int k = 0; k < NK; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+}
+
 template <int DEPTH, bool U32, int DPL = 4>
 __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes, const Lane &ln,
                                             int warp, int nk, Acc<U32, DPL> &acc)
@@ -872,19 +880,20 @@ __device__ __forceinline__ void apply_chunk(uint32_t chunk, uint32_t desc_bytes,
     // chunks hold nk * 16 trees (the last one padded with zero-answer trees).
     // (A software pipeline loading the next pair's descriptors during this pair was
     // slower: c3 fused 6.43 -> 7.66 ms.)
-    // a multiple of 4 trees per warp runs 4 trees per iteration (warp-uniform choice)
+    // a multiple of 4 trees per warp runs 4 trees per iteration; 6 (c3's 96-tree
+    // chunks) all at once.  (A switch fully unrolling 3..8 trees measured slower on
+    // c3: 6.44 / 6.46 ms, larger code; so only these two shapes.)
     if (DEPTH <= 6 && (nk & 3) == 0) {
 #pragma unroll 4
         for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
-#if ODF_UNROLL3
-    } else if (DEPTH <= 6 && nk % 3 == 0) {  // e.g. c3: 96-tree chunks, 6 trees per warp
-#pragma unroll 3
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
-#endif
-    } else {
-#pragma unroll kApplyUnroll
-        for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
+        return;
     }
+    if (DEPTH <= 6 && nk == 6) {
+        apply_trees_all<DEPTH, U32, DPL, 6>(chunk, desc_bytes, ln, warp, acc);
+        return;
+    }
+#pragma unroll kApplyUnroll
+    for (int k = 0; k < nk; ++k) apply_tree<DEPTH, U32, DPL>(chunk, desc_bytes, ln, warp + k * kConsumerWarps, acc);
 }
 
 // Fixed-order combine of the 16 group partials of document tid (< tile_docs) and store:
