@@ -149,6 +149,10 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sabs(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(sabs(bar)), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
     asm volatile(
@@ -966,7 +970,7 @@ __device__ __forceinline__ void expand_wide(const KParams &p, uint32_t stage, ui
 // arrays.  Warp w binarizes quad w >> 1 of every box for documents 64 * (w & 1) +
 // lane (+ 32); the codes of half h go to the code block at h * half_stride.  Only
 // the tile's hv halves that hold documents are loaded and binarized.
-template <bool CODES, bool WIDE, bool FM, int H, class Sink, int DPL = 4>
+template <bool CODES, bool WIDE, bool FM, int H, class Sink, int DPL = 4, bool SPLIT2 = false>
 __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint32_t ring, uint32_t bars,
                                         int n_fjobs, int S, int warp, int lane, uint32_t &slot,
                                         uint32_t &ph, unsigned long long &wait_ns, int hv)
@@ -978,6 +982,34 @@ __device__ __forceinline__ void phase_a(const KParams &p, const Sink sink, uint3
     const int fsub = p.fsub_per_job, n_fchunks = p.n_fchunks;
     const uint32_t slot_bytes = p.slot_bytes, off_meta = p.off_meta, off_bord = p.off_bord,
                    bord_stride = p.bord_stride;
+    // SPLIT2 (fused, 128-document tiles, one half; deep forests): warps 8h..8h+7
+    // binarize the jobs j with j % 2 == h, warp w quad w & 7 for all 128 documents (4 per
+    // lane): two jobs in progress at once and twice the work per job set-up; each warp
+    // of the half arrives twice on the job's empty barrier (16 arrivals).  c4 (depth 10,
+    // two-sub-tile jobs): fused 28.2 -> 26.4 ms; at depth 6 it costs more than it saves
+    // (c3 6.14 -> 6.59 ms, c2 0.244 -> 0.250 ms), so only depth >= 7 uses it.
+    if constexpr (SPLIT2 && CODES && H == 1 && DPL == 4) {
+        const int q2 = warp & 7, half = warp >> 3;
+        for (int j = 0; j < n_fjobs; ++j) {
+            if ((j & 1) == half) {
+                const uint32_t full = bars + 16u * slot, empty = full + 8u;
+                mbar_wait(full, ph);
+                const int nsub = min(fsub, n_fchunks - j * fsub);
+                const uint32_t sb = ring + slot * slot_bytes;
+                for (int s = 0; s < nsub; ++s)
+                    binarize_sub<4, CODES, WIDE, FM, Sink, 0>(sb + s * kBox, sb + off_meta + s * kMetaBytes,
+                                                             sb + off_bord + s * bord_stride, sink, q2, 0, lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cnt(empty, 2);
+            }
+            if (++slot == static_cast<uint32_t>(S)) {
+                slot = 0;
+                ph ^= 1u;
+            }
+        }
+        (void)wait_ns;
+        return;
+    }
     const int q = warp >> 1, dbase = (warp & 1) * 32 * NDL;
     for (int j = 0; j < n_fjobs; ++j) {
         const uint32_t full = bars + 16u * slot, empty = full + 8u;
@@ -1205,10 +1237,10 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         } else if (HAS_A) {
             {
                 if (p.fm)
-                    phase_a<MODE == MODE_FUSED, WIDE, true, H, SmemSink, DPL>(p, SmemSink{bins}, ring, bars, n_fjobs,
+                    phase_a<MODE == MODE_FUSED, WIDE, true, H, SmemSink, DPL, (DEPTH >= 7 && !MIXED)>(p, SmemSink{bins}, ring, bars, n_fjobs,
                                                                               S, warp, lane, slot, ph, waitA, hv);
                 else
-                    phase_a<MODE == MODE_FUSED, WIDE, false, H, SmemSink, DPL>(p, SmemSink{bins}, ring, bars, n_fjobs,
+                    phase_a<MODE == MODE_FUSED, WIDE, false, H, SmemSink, DPL, (DEPTH >= 7 && !MIXED)>(p, SmemSink{bins}, ring, bars, n_fjobs,
                                                                                S, warp, lane, slot, ph, waitA, hv);
             }
         }
