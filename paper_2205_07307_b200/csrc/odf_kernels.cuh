@@ -848,6 +848,9 @@ struct Acc<true, DPL> {
     }
 };
 
+#ifndef ODF_SPLIT_MIN_DEPTH
+#define ODF_SPLIT_MIN_DEPTH 7  // A/B builds: smallest depth whose fused phase A uses the warp-half split
+#endif
 #ifndef ODF_APPLY_UNROLL
 #define ODF_APPLY_UNROLL 2
 #endif
@@ -1237,10 +1240,10 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         } else if (HAS_A) {
             {
                 if (p.fm)
-                    phase_a<MODE == MODE_FUSED, WIDE, true, H, SmemSink, DPL, (DEPTH >= 7 && !MIXED)>(p, SmemSink{bins}, ring, bars, n_fjobs,
+                    phase_a<MODE == MODE_FUSED, WIDE, true, H, SmemSink, DPL, (DEPTH >= ODF_SPLIT_MIN_DEPTH && !MIXED)>(p, SmemSink{bins}, ring, bars, n_fjobs,
                                                                               S, warp, lane, slot, ph, waitA, hv);
                 else
-                    phase_a<MODE == MODE_FUSED, WIDE, false, H, SmemSink, DPL, (DEPTH >= 7 && !MIXED)>(p, SmemSink{bins}, ring, bars, n_fjobs,
+                    phase_a<MODE == MODE_FUSED, WIDE, false, H, SmemSink, DPL, (DEPTH >= ODF_SPLIT_MIN_DEPTH && !MIXED)>(p, SmemSink{bins}, ring, bars, n_fjobs,
                                                                                S, warp, lane, slot, ph, waitA, hv);
             }
         }
