@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--only", default="all")
     ap.add_argument("--n-docs", type=int, default=None)
+    ap.add_argument("--tile-docs", type=int, default=0, help="128 / 256 (0: automatic)")
     a = ap.parse_args()
     import torch
     import synth
@@ -32,11 +33,11 @@ def main():
     bins = torch.empty(m.bins_bytes(n), dtype=torch.uint8, device="cuda")
     for _ in range(a.iters):
         if a.only in ("all", "fused"):
-            m.score(x, out=out)
+            m.score(x, out=out, tile_docs=a.tile_docs)
         if a.only in ("all", "binarize", "apply"):
             m.binarize(x, out=bins)
         if a.only in ("all", "apply"):
-            m.apply(bins, n, out=out)
+            m.apply(bins, n, out=out, tile_docs=a.tile_docs)
     torch.cuda.synchronize()
     print("done", flush=True)
 
