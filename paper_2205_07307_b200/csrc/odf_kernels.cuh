@@ -580,8 +580,9 @@ __device__ __forceinline__ void binarize_sub(uint32_t tile, uint32_t meta, uint3
 // FALSE.  Flags are shifted in from the top of each byte, so after DEPTH levels
 // level l sits at bit 8-DEPTH+l: the byte is the complemented leaf index F,
 // and leaf tables are stored reversed (table[F] = leaf[2^d-1-F]).
-// Descriptors are 4 bytes per level (odf_internal.h): 6 levels cost one LDS.128
-// and one LDS.64 broadcast instead of three LDS.128.
+// Descriptors (odf_internal.h): depth <= 8 the split format (column words, then the
+// K bytes packed four per word: a depth-6 tree is 32 B = two warp-uniform LDS.128);
+// depth 9-10 one 4-byte word per level.
 // A lane's view of a tile's code block: the absolute address of its 4 documents'
 // bytes in code column 0.
 struct Lane {
