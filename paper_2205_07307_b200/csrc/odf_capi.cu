@@ -776,9 +776,23 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         const uint32_t nleaf = 1u << sdepth;
         const float *lf = static_cast<const float *>(g.leaves);
         const uint32_t *lu = static_cast<const uint32_t *>(g.leaves);
-        for (int64_t t = 0; t < g.n_trees; ++t) {
-            uint8_t *ch = chunks.data() + base + static_cast<size_t>(t / tc) * cbytes;
-            const int64_t i = t % tc;
+#ifdef ODF_TREE_SORT  // A/B timing builds only (P:434 locality reordering): trees sorted by their level features
+        std::vector<int64_t> order(static_cast<size_t>(g.n_trees));
+        for (int64_t t = 0; t < g.n_trees; ++t) order[t] = t;
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b2) {
+            for (int l = 0; l < sdepth; ++l)
+                if (g.fi[a * sdepth + l] != g.fi[b2 * sdepth + l]) return g.fi[a * sdepth + l] < g.fi[b2 * sdepth + l];
+            return false;
+        });
+#endif
+        for (int64_t pos = 0; pos < g.n_trees; ++pos) {
+#ifdef ODF_TREE_SORT
+            const int64_t t = order[pos];
+#else
+            const int64_t t = pos;
+#endif
+            uint8_t *ch = chunks.data() + base + static_cast<size_t>(pos / tc) * cbytes;
+            const int64_t i = pos % tc;
             uint32_t *desc = reinterpret_cast<uint32_t *>(ch + i * dstride);
             for (int l = 0; l < sdepth; ++l) {
                 const int32_t f = g.fi[t * sdepth + l];
