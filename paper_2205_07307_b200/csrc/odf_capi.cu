@@ -90,6 +90,10 @@ struct Plan {
     bool valid = false;
 };
 
+#ifndef ODF_TAIL64
+#define ODF_TAIL64 1  // A/B builds: 0 keeps the partly filled last wave in 128-document tiles
+#endif
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -125,6 +129,7 @@ struct odf_model {
     double scale = 1.0, bias = 0.0;
     Plan fused, binz, apply;
     Plan fused2, apply2;  // 256-document tiles (two halves), when they fit
+    Plan fused64;         // 64-document tiles for a partly filled last wave (odf_score_tiles)
     // odf_score_host staging
     std::mutex host_mu;
     float *d_stage[2] = {nullptr, nullptr};
@@ -139,14 +144,14 @@ namespace {
 // ----------------------------------------------------------------------------
 // shared-memory plans
 // ----------------------------------------------------------------------------
-bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int halves = 1)
+bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int halves = 1, int tile_docs = 0)
 {
     // code columns + the trash column (stores of unused pair slots), one block per
     // tile half; the binarize kernel of a wide model stores u16 bins; the apply kernel
     // of a wide model stages the u16 bins tile next to the code columns it expands
     // them into
     const uint32_t elem = (mode == MODE_BINARIZE && m.wide) ? 2u : 1u;
-    const uint32_t td = static_cast<uint32_t>(m.tile_docs);  // documents per tile (half)
+    const uint32_t td = static_cast<uint32_t>(tile_docs ? tile_docs : m.tile_docs);  // documents per tile (half)
     const uint32_t half_bins = align_up(static_cast<uint64_t>(m.n_cols + 1) * td * elem, 1024);
     const uint32_t bins = half_bins * static_cast<uint32_t>(halves);
     const uint32_t stage = (mode == MODE_APPLY && m.wide)
@@ -211,7 +216,7 @@ bool make_plan(const odf_model &m, int mode, Plan &pl, std::string &why, int hal
 }
 
 odf_status encode_tmap(const odf_model *m, const float *d_x, int64_t n_docs, int64_t ld,
-                       CUtensorMap *tm, bool fm = false)
+                       CUtensorMap *tm, bool fm = false, int tile_docs = 0)
 {
     std::call_once(g_encode_once, [] {
         void *fn = nullptr;
@@ -227,7 +232,7 @@ odf_status encode_tmap(const odf_model *m, const float *d_x, int64_t n_docs, int
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(fm ? n_docs : m->n_features),
                           static_cast<cuuint64_t>(fm ? m->n_features : n_docs)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-    const cuuint32_t td = static_cast<cuuint32_t>(m->tile_docs);  // documents per tile
+    const cuuint32_t td = static_cast<cuuint32_t>(tile_docs ? tile_docs : m->tile_docs);  // documents per tile
     cuuint32_t box[2] = {static_cast<cuuint32_t>(fm ? td : kFSub), static_cast<cuuint32_t>(fm ? kFSub : td)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(d_x), dims,
@@ -919,6 +924,7 @@ static odf_status load_model_core(const odf_model_desc *desc, const std::vector<
         if (!make_plan(*m, MODE_FUSED, m->fused2, why2, 2)) m->fused2 = Plan();
         if (!make_plan(*m, MODE_APPLY, m->apply2, why2, 2)) m->apply2 = Plan();
         if (!m->fused2.valid || !m->apply2.valid) m->fused2 = m->apply2 = Plan();  // both or neither
+        if (!make_plan(*m, MODE_FUSED, m->fused64, why2, 1, kTile / 2)) m->fused64 = Plan();
     }
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -971,16 +977,22 @@ odf_status odf_bins_layout(const odf_model *m, int64_t n_docs, size_t *bytes,
     return ok();
 }
 
+// pdl: 0 plain launch; 1 primary of a programmatic dependent launch; 2 its secondary, run
+// with the 64-document-tile plan (m->fused64) on a partly filled last wave
 static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64_t n_docs, int64_t ld,
                            const uint8_t *bins_in, uint8_t *bins_out, float *scores, cudaStream_t s,
                            uint64_t *sums = nullptr, double *dscores = nullptr, bool fm = false,
-                           int halves = 1)
+                           int halves = 1, int pdl = 0)
 {
-    const Plan &pl = halves == 2 ? (mode == MODE_FUSED ? m->fused2 : m->apply2)
-                                 : mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
+    const Plan &pl = pdl == 2 ? m->fused64
+                     : halves == 2 ? (mode == MODE_FUSED ? m->fused2 : m->apply2)
+                                   : mode == MODE_FUSED ? m->fused : mode == MODE_APPLY ? m->apply : m->binz;
     KParams p = base_params(m, pl);
+    const int td = pdl == 2 ? kTile / 2 : m->tile_docs;
+    p.tile_docs = td;
+    p.pdl = pdl;
     p.n_docs = n_docs;
-    p.n_tiles = (n_docs + m->tile_docs * halves - 1) / (m->tile_docs * halves);
+    p.n_tiles = (n_docs + td * halves - 1) / (td * halves);
     p.bins_in = bins_in;
     p.bins_out = bins_out;
     p.scores = scores;
@@ -990,7 +1002,7 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     const CUtensorMap *tmp = nullptr;
     p.fm = fm ? 1 : 0;
     if (mode != MODE_APPLY && p.n_fchunks > 0) {
-        odf_status st = encode_tmap(m, d_x, n_docs, ld, &tm, fm);
+        odf_status st = encode_tmap(m, d_x, n_docs, ld, &tm, fm, td);
         if (st != ODF_OK) return st;
         tmp = &tm;
     }
@@ -998,7 +1010,7 @@ static odf_status run_main(const odf_model *m, int mode, const float *d_x, int64
     cudaGetDevice(&prev);
     if (prev != m->device) cudaSetDevice(m->device);
     cudaError_t e = launch_main(mode, mode == MODE_BINARIZE ? 0 : m->kdepth, p, tmp,
-                                grid_for(m, pl, p.n_tiles), pl.smem, s, halves);
+                                grid_for(m, pl, p.n_tiles), pl.smem, s, halves, pdl == 2);
     if (prev != m->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     return ok();
@@ -1057,6 +1069,20 @@ odf_status odf_score_tiles(const odf_model *m, const float *d_factors, int64_t n
     if (!halves) return st;
     if (n_docs == 0) return ok();
     if (!d_scores) return fail(ODF_E_INVALID_ARG, "d_scores is NULL");
+    // A last wave of 128-document tiles at most half full runs as 64-document tiles on twice
+    // as many SMs, launched programmatically so it starts as the full waves' CTAs retire
+    // (same per-document summation order: bit-identical scores).
+    const int64_t nt = (n_docs + kTile - 1) / kTile, S = m->num_sms;
+    if (ODF_TAIL64 && tile_docs == 0 && halves == 1 && m->fused64.valid && nt > S && nt % S != 0 &&
+        2 * (nt % S) <= S) {
+        const int64_t n1 = nt / S * S * kTile;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        st = run_main(m, MODE_FUSED, d_factors, n1, ld, nullptr, nullptr, d_scores, s, nullptr, nullptr, false,
+                      1, 1);
+        if (st != ODF_OK) return st;
+        return run_main(m, MODE_FUSED, d_factors + n1 * ld, n_docs - n1, ld, nullptr, nullptr, d_scores + n1, s,
+                        nullptr, nullptr, false, 1, 2);
+    }
     return run_main(m, MODE_FUSED, d_factors, n_docs, ld, nullptr, nullptr, d_scores,
                     static_cast<cudaStream_t>(stream), nullptr, nullptr, false, halves);
 }

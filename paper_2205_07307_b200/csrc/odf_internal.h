@@ -107,6 +107,8 @@ struct KParams {
     SegP seg[kMaxSegments];
     // ---- problem ----
     int32_t tile_docs;       // the model's tile width: 128, or 64 (wide-column models, DPL = 2)
+    int32_t pdl;             // 1: primary of a programmatic dependent launch (lets the secondary
+                             // launch), 2: secondary (waits for the primary before it exits)
     int64_t n_docs, n_tiles;
     const uint8_t *bins_in;  // blocked bins (apply / index kernels)
     uint8_t *bins_out;       // blocked bins (binarize)
@@ -160,7 +162,8 @@ const void *kptr_apply_h2(int depth);  // apply, fp32 leaves, 256-document tiles
 const void *kptr_binarize(bool wide);
 
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
-                        size_t smem, cudaStream_t s, int halves = 1);  // p.tile_docs picks DPL
+                        size_t smem, cudaStream_t s, int halves = 1,
+                        bool pdl_secondary = false);  // p.tile_docs picks DPL
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,
                          cudaStream_t s);
 cudaError_t launch_latency(int depth, const KParams &p, const CUtensorMap *tmap, int splits,

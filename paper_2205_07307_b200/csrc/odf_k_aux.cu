@@ -185,7 +185,7 @@ int occupancy_main(int mode, int depth, size_t smem, int tile_docs)
 }
 
 cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap *tmap, int grid,
-                        size_t smem, cudaStream_t s, int halves)
+                        size_t smem, cudaStream_t s, int halves, bool pdl_secondary)
 {
     const void *f = main_kernel(mode, depth, p.leaf_u32 != 0, p.wide != 0, halves, p.tile_docs);
     if (!f) return cudaErrorInvalidValue;
@@ -196,7 +196,19 @@ cudaError_t launch_main(int mode, int depth, const KParams &p, const CUtensorMap
     else
         memset(&tm, 0, sizeof(tm));
     void *args[] = {&pc, &tm};
-    return cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, s);
+    if (!pdl_secondary) return cudaLaunchKernel(f, dim3(grid), dim3(kThreads), args, smem, s);
+    // programmatic dependent launch: may start while the primary (same stream) runs
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, f, args);
 }
 
 cudaError_t launch_index(int depth, const KParams &p, bool fingerprint, int grid, size_t smem,

@@ -1120,6 +1120,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
     if (HAS_A)
         for (int c = threadIdx.x; c < p.n_fchunks; c += kThreads) sst<uint2>(bct + 8u * c, p.bchunk[c]);
     __syncthreads();
+    // partly filled last wave (odf_score_tiles): the 64-document-tile secondary launch may
+    // start as soon as SMs free up
+    if (p.pdl == 1 && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == kConsumerWarps) {
         // ===================== producer warp (one elected lane) =====================
@@ -1345,6 +1348,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BINARIZE ? 2 : 1)  // K
         ++diag_it;
 #endif
     }
+    // secondary of a programmatic dependent launch: complete only after the primary, so
+    // later stream work sees both grids' scores
+    if (p.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
