@@ -7,7 +7,7 @@
 namespace odf {
 cudaError_t prepare_kernels(int) { return cudaErrorNotSupported; }
 int occupancy_main(int, int, size_t, int) { return 1; }
-cudaError_t launch_main(int, int, const KParams &, const CUtensorMap *, int, size_t, cudaStream_t, int)
+cudaError_t launch_main(int, int, const KParams &, const CUtensorMap *, int, size_t, cudaStream_t, int, bool)
 {
     return cudaErrorNotSupported;
 }
