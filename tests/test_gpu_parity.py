@@ -853,3 +853,30 @@ def test_many_columns_fp32_tolerance(n_docs):
     two-stage bit for bit."""
     case = _many_column_case(6, n_docs=n_docs, exact=False)
     full_check(case)
+
+
+@pytest.mark.parametrize("extra_tiles,tail", [(1, 0), (20, 37), (74, 0), (75, 5)])
+def test_partial_last_wave_as_64_document_tiles(extra_tiles, tail):
+    """odf_score's partly filled last wave (<= half of the SMs) runs as 64-document tiles
+    in a programmatic dependent launch: bit-identical to 128-document tiles throughout
+    (tile_docs=128 never splits) and to the two-stage path, and bit-exact against the
+    oracle with exact-arithmetic leaves; 75 extra tiles (> half) keep one launch."""
+    import torch
+    probe = cuda_model(synth.tiny_case(seed=91, n_docs=128, n_features=40, n_trees=64, depth=6, pool=24))
+    sms = probe.info["num_sms"]
+    probe.close()
+    n_docs = (sms + extra_tiles) * 128 + tail
+    case = synth.tiny_case(seed=90 + extra_tiles, n_docs=n_docs, n_features=40, n_trees=96, depth=6, pool=24,
+                           exact_leaves=True)
+    m = cuda_model(case)
+    x = to_dev(case.x)
+    auto = m.score(x)
+    t128 = m.score(x, tile_docs=128)
+    two = m.apply(m.binarize(x), n_docs)
+    torch.cuda.synchronize()
+    _, s32 = oracle.score(case.x, case.feature_index, case.thresholds, case.leaf_values, case.depth)
+    a = auto.cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), t128.cpu().numpy().view(np.uint32))
+    assert np.array_equal(a.view(np.uint32), two.cpu().numpy().view(np.uint32))
+    assert np.array_equal(a, s32)
+    m.close()
