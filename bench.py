@@ -361,6 +361,7 @@ def run_ours(args):
     x_host = case.x[lo - off:hi - off]
     x = torch.from_numpy(np.ascontiguousarray(x_host)).to(dev)
     n = x.shape[0]
+    launches_per_step = model.score_launches(n)  # 2 when the last wave runs as a second grid
     out = torch.empty(n, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     ds = DocSharded(lambda t: model.score(t))
@@ -494,7 +495,7 @@ def run_ours(args):
                     "path": "odf_score_host (pinned host memory, chunked H2D/score/D2H)"
                             + (" on every rank" if weak else "")
                             if ws == 1 or weak else "H2D + odf_score + NCCL collective + D2H on rank 0"},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clk.summary(),
             "model": {k: info[k] for k in ("n_split_features", "n_columns", "trees_per_chunk",
                                            "stages_fused", "smem_fused", "total_borders",

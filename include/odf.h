@@ -167,6 +167,8 @@ typedef struct {
                                    for models whose 128-document code block does not fit shared
                                    memory (about > 1,600 code columns, e.g. P:168's 1,950 factors;
                                    at depth 9-10 such widths do not fit at all: ODF_E_UNSUPPORTED) */
+    int32_t tail_tile_docs;     /* 64 if odf_score runs a partly filled last wave as 64-document tiles
+                                   (a second grid, odf_score_tiles), else 0 */
 } odf_model_info;
 
 ODF_API odf_status odf_get_info(const odf_model *m, odf_model_info *info);

@@ -961,6 +961,7 @@ odf_status odf_get_info(const odf_model *m, odf_model_info *info)
     info->bins_tile_docs = m->tile_docs;
     info->stages_fused_256 = m->fused2.valid ? m->fused2.stages : 0;
     info->smem_fused_256 = m->fused2.valid ? static_cast<int32_t>(m->fused2.smem) : 0;
+    info->tail_tile_docs = (ODF_TAIL64 && m->fused64.valid) ? kTile / 2 : 0;
     return ok();
 }
 

@@ -43,7 +43,7 @@ class _Info(ctypes.Structure):
                 ("leaf_type", ctypes.c_int32), ("bord_stride", ctypes.c_int32),
                 ("bins_elem_bytes", ctypes.c_int32), ("max_tile_docs", ctypes.c_int32),
                 ("stages_fused_256", ctypes.c_int32), ("smem_fused_256", ctypes.c_int32),
-                ("bins_tile_docs", ctypes.c_int32)]
+                ("bins_tile_docs", ctypes.c_int32), ("tail_tile_docs", ctypes.c_int32)]
 
 
 class _Desc(ctypes.Structure):
@@ -275,6 +275,14 @@ class Model:
     # -- helpers ----------------------------------------------------------
     def _dev(self):
         return torch.device("cuda", self.device)
+
+    def score_launches(self, n_docs: int) -> int:
+        """Kernel launches of one odf_score (tile_docs = 0) over n_docs documents: 2 when a
+        partly filled last wave runs as 64-document tiles in a second grid (odf.h)."""
+        if not self.info.get("tail_tile_docs") or n_docs <= 0:
+            return 1 if n_docs > 0 else 0
+        nt, s = (n_docs + 127) // 128, self.info["num_sms"]
+        return 2 if nt > s and nt % s and 2 * (nt % s) <= s else 1
 
     def bins_bytes(self, n_docs: int) -> int:
         nb = ctypes.c_size_t()
