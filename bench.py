@@ -292,12 +292,18 @@ def _secondary(cfg, steps, warmup, dev, stream):
     out = torch.empty(case.n_docs, dtype=torch.float32, device=dev)
     for _ in range(warmup):
         m.score(x, out=out, stream=stream)
-    total_ms, kern_ms = _time_steps(lambda: m.score(x, out=out, stream=stream), steps, stream, 1, dev)
+    with ClockSampler(dev.index) as ck:
+        total_ms, kern_ms = _time_steps(lambda: m.score(x, out=out, stream=stream), steps, stream, 1, dev)
     n_used = m.info["n_used_features"]
+    clocks = ck.summary()
     res = {"workload": synth.WORKLOAD_NAMES[cfg], "value": case.n_docs * steps / (total_ms / 1e3),
            "unit": "docs/s", "ms_per_step": total_ms / steps, "steps": steps,
            "doc_trees_per_s": case.n_docs * case.n_trees * steps / (total_ms / 1e3),
-           "roofline": _roofline_hbm(case.n_docs, n_used, kern_ms, cfg)}
+           "roofline": _roofline_hbm(case.n_docs, n_used, kern_ms, cfg),
+           "roofline_binding": _roofline_smem(cfg, kern_ms, m.info["num_sms"],
+                                              clocks.get("sm_mhz") or ck.max_mhz or 1965),
+           "gpu_launches": steps * m.score_launches(case.n_docs),
+           "clocks": clocks}
     m.close()
     return res
 
@@ -514,11 +520,17 @@ def run_ours(args):
                                  "docs_per_s": n / ((tb + ta) / 1000.0),
                                  "binarize_hbm_frac": n * 5 * nu / (tb / 1e3) / 1e9 / hbm,
                                  "binarize_alg_bytes_per_doc": 5 * nu}
-        if ws == 1 and args.secondary != "none" and args.secondary != args.config:
+        sec = [c for c in args.secondary.split(",") if c and c != "none" and c != args.config]
+        if ws == 1 and sec:
             del x
             torch.cuda.empty_cache()
-            line["secondary"] = _secondary(args.secondary, max(3, min(args.steps * 10, 500)),
+            # the first (c2) is `secondary`; the deep forest (c4) `secondary_deep`, fewer steps
+            line["secondary"] = _secondary(sec[0], max(3, min(args.steps * 10, 500)),
                                            max(3, args.warmup), dev, stream)
+            for c in sec[1:]:
+                torch.cuda.empty_cache()
+                line["secondary_deep" if c == "c4" else f"secondary_{c}"] = _secondary(
+                    c, max(3, min(args.steps, 20)), max(3, args.warmup), dev, stream)
         if not args.no_cpu_baseline and ws == 1:  # the oracle baseline: rank 0 at N=1 only
             line["cpu_baseline"] = cpu_baseline(case, target_s=args.ref_seconds)
         print(json.dumps(line), flush=True)
@@ -543,7 +555,8 @@ def main():
     ap.add_argument("--weak", action="store_true",
                     help="multi-GPU: every rank scores its own full batch (same model, its own seed), "
                          "no collective on the data path (weak scaling)")
-    ap.add_argument("--secondary", default="c2", help="second workload reported in the line, or none")
+    ap.add_argument("--secondary", default="c2,c4",
+                    help="further workloads reported in the line (comma list), or none")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunk", type=int, default=65536)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
