@@ -2,14 +2,15 @@
 """Benchmark of the oblivious-forest hot path (binarize + apply) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--shard docs|trees]
-                    [--weak] [--impl ours|reference] [--secondary c2|none]
+                    [--weak] [--impl ours|reference] [--secondary c2,c4|none]
 
 One "step" = one pass of the whole hot path (the fused odf_score kernel:
 binarization + leaf-index assembly + leaf gather/sum) over one
 synthetic batch.  The headline workload is BASELINE.json configs[2] = c3, the
 1,000,000-document config the north_star's HBM target names (1,000,000 docs x
-1,000 factors, 10,000 depth-6 trees); c2 (configs[1]) is reported alongside in
-the same run as a secondary object.  Inputs are resident in HBM when the timed
+1,000 factors, 10,000 depth-6 trees); c2 (configs[1]) and the deep forest c4
+(configs[3]) are reported alongside in the same run (`secondary`, `secondary_deep`,
+each with its own NVML clocks).  Inputs are resident in HBM when the timed
 region starts and larger than L2 (4 GB vs 126 MB), so no L2 flush is needed.
 
 N > 1 (torchrun, one rank per GPU, NCCL):
