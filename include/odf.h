@@ -213,8 +213,9 @@ ODF_API odf_status odf_score(const odf_model *m, const float *d_factors, int64_t
  * still has >= 3 slots, stages_fused_256).  Scores are bit-identical for
  * every tile width (the summation order of DESIGN.md does not depend on it).
  * Models with odf_model_info.bins_tile_docs == 64 run 64-document tiles only
- * (tile_docs 0 or 64).  With tile_docs = 0, odf_score also runs a last wave of
- * 128-document tiles that would fill at most half of the SMs as 64-document tiles
+ * (tile_docs 0 or 64).  With tile_docs = 0, odf_score (fp32 uniform models of depth
+ * <= 6) also runs a last wave of 128-document tiles that would fill at most half of
+ * the SMs as 64-document tiles
  * in a second grid (a programmatic dependent launch on the same stream; the call
  * still enqueues one unit of work: later work on the stream sees every score).
  * Errors: as odf_score / odf_apply; ODF_E_INVALID_ARG for another tile_docs;

@@ -14,9 +14,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def metrics(rep):
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_metrics.py"), rep],
+    """Counters of the report's launches, summed (odf_score may run a second grid for a
+    partly filled last wave: both belong to one launch of the fused path)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_metrics.py"), rep, "--all"],
                          capture_output=True, text=True, check=True).stdout
-    m = json.loads(out)
+    ms = json.loads(out)
+    m = dict(ms[0])
+    for extra in ms[1:]:
+        for k in ("duration_ms", "dram_read", "dram_write", "xbar2l1tex_bytes", "smem_ld_wavefronts",
+                  "smem_st_wavefronts", "smem_bank_conflicts_ld", "warp_instructions"):
+            if extra.get(k) is not None and m.get(k) is not None:
+                m[k] += extra[k]
+        m["kernel"] += " + " + extra["kernel"][:40]
     return {
         "kernel": m["kernel"],
         "dram_bytes_per_launch": int(m["dram_read"] + m["dram_write"]),
